@@ -1,0 +1,422 @@
+"""Benchmark of the Star Attention two-phase hot path on B200.
+
+Workload (BASELINE.json configs[1], the metric's own config): Llama-3.1-8B
+attention shapes — 32 q / 8 kv heads, head_dim 128 — over a 128K context cut
+into 16K blocks with 16K first-block anchors, bf16, one layer per step.
+
+One step = phase 1 of one layer over the whole context: RoPE of Q and K at the
+augmented position ids, the tcgen05 causal block encode (K1) over every
+anchor-augmented block this rank owns, and the own-row K/V write into the paged
+cache.  `value` = context tokens encoded per second over all ranks (strong
+scaling: the 128K context is fixed, blocks are sharded by partition()).
+After the timed steps, the per-token phase-2 decode latency (K2 split-KV
+partial over the rank's paged cache + NCCL all-gather of (out, lse) + K3
+merge) is measured the same way and reported under "decode".
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "context-encode tokens/s & per-token decode latency (128K ctx), 1–8 B200"
+CFG = dict(L=131072, b=16384, a=16384, hq=32, hkv=8, d=128, seed=0)
+
+
+def star_pairs(L, b, a):
+    n = -(-L // b)
+    return sum((m := (min(b, L - i * b) + (a if i else 0))) * (m + 1) // 2 for i in range(n))
+
+
+def rank_blocks(L, b, a, G, rank):
+    """(block index, augmented rows m_i, own rows) for the blocks partition() gives `rank`."""
+    n = -(-L // b)
+    owner = [min(i * G // n, G - 1) for i in range(n)]
+    out = []
+    for i in range(n):
+        if owner[i] == rank:
+            own = min(b, L - i * b)
+            out.append((i, own + (a if i else 0), own))
+    return out
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_sample(rows=8192, reps=None, budget_s=12.0):
+    """Time the oracle's causal_attention (numpy restatement of ss/attention.py:109-122) on
+    one (q-head, `rows`-row block) unit, fp32, d=128, repeated until ~budget_s."""
+    from oracle import star_oracle as O
+
+    d = CFG["d"]
+    q = O.counter_fill(1, rows * d).astype(np.float32).reshape(rows, d)
+    k = O.counter_fill(2, rows * d).astype(np.float32).reshape(rows, d)
+    v = O.counter_fill(3, rows * d).astype(np.float32).reshape(rows, d)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while (reps is None and (time.perf_counter() < t_end or not times)) or (reps is not None and len(times) < reps):
+        t0 = time.perf_counter()
+        O.causal_attention(q, k, v)
+        times.append(time.perf_counter() - t0)
+    return float(np.median(times)), rows, len(times)
+
+
+def cpu_tokens_per_s(t_unit, rows):
+    """Extrapolate one (head, rows) unit to the whole cfg2 layer by score-pair count."""
+    pairs_total = star_pairs(CFG["L"], CFG["b"], CFG["a"]) * CFG["hq"]
+    unit_pairs = rows * (rows + 1) // 2
+    return CFG["L"] / (t_unit * pairs_total / unit_pairs)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_sample(reps=1)
+    ts = []
+    for _ in range(args.steps):
+        t, rows, _ = cpu_sample(reps=1)
+        ts.append(t)
+    t = float(np.median(ts))
+    val = cpu_tokens_per_s(t, rows)
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (splitmix64 counter fill)",
+        "config": {"workload": "cfg2 phase-1 encode, one layer", "context": CFG["L"],
+                   "block": CFG["b"], "anchor": CFG["a"], "heads_q": CFG["hq"],
+                   "heads_kv": CFG["hkv"], "head_dim": CFG["d"], "parallelism": f"star{args.gpus}"},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle causal_attention, one q-head x {rows}-row block per step, "
+                                   "extrapolated by score pairs to 32 heads x 8 blocks"},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_17116_b200 import ops
+    from paper_2411_17116_b200.numerics import Prng  # noqa: F401  (API import check)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    G = world
+    L, b, a, hq, hkv, d, seed = (CFG[k] for k in ("L", "b", "a", "hq", "hkv", "d", "seed"))
+    blocks = rank_blocks(L, b, a, G, rank)
+    seg = [0]
+    pos_list = []
+    for i, m, own in blocks:
+        seg.append(seg[-1] + m)
+        start = i * b
+        pos_list.append(np.concatenate([np.arange(a), np.arange(start, start + own)]) if i
+                        else np.arange(start, start + own))
+    R = seg[-1]
+    positions = torch.from_numpy(np.concatenate(pos_list).astype(np.int64)).to(dev)
+
+    # synthetic pre-RoPE Q/K/V: row r of an augmented block is context row positions[r]
+    # (first_block anchors repeat block 0's rows), drawn from splitmix64 counter streams
+    def ctx_gather(seed_x, heads):
+        full = ops.prng_fill((L, heads, d), seed_x, 1, 1.0, torch.bfloat16, dev)
+        return full.index_select(0, positions).contiguous()
+
+    q_raw = ctx_gather(seed ^ 1, hq)
+    k_raw = ctx_gather(seed ^ 2, hkv)
+    v = ctx_gather(seed ^ 3, hkv)
+    q_rot = torch.empty_like(q_raw)
+    k_rot = torch.empty_like(k_raw)
+    out = torch.empty_like(q_raw)
+    own_rows = sum(o for _, _, o in blocks)
+    page = 128
+    n_pages = -(-own_rows // page) + 1
+    kpool = torch.zeros((n_pages, hkv, page, d), dtype=torch.bfloat16, device=dev)
+    vpool = torch.zeros_like(kpool)
+    table = torch.arange(n_pages, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    launches = [0]
+
+    def step(qr, kr, vv, o, k1_events=None):
+        ops.rope(qr, positions, 10000.0, out=q_rot)
+        ops.rope(kr, positions, 10000.0, out=k_rot)
+        if k1_events is not None:
+            k1_events[0].record(stream)
+        ops.phase1_fwd(q_rot, k_rot, vv, seg, out=o)
+        if k1_events is not None:
+            k1_events[1].record(stream)
+        row0 = 0
+        for (i, m, own), s0 in zip(blocks, seg[:-1]):
+            lo = s0 + (m - own)
+            ops.kv_write(k_rot[lo:lo + own], vv[lo:lo + own], kpool, vpool, table, row0)
+            row0 += own
+        launches[0] += 3 + len(blocks)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- device-resident timing (value) ----------------
+    for _ in range(args.warmup):
+        step(q_raw, k_raw, v, out)
+    barrier()
+    k1_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(args.steps)]
+    launches[0] = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for s in range(args.steps):
+            step(q_raw, k_raw, v, out, k1_ev[s])
+        e1.record(stream)
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    k1_ms = max_over_ranks(float(np.mean([x.elapsed_time(y) for x, y in k1_ev])))
+    gpu_launches = launches[0]
+    value = L / (ms * 1e-3)
+
+    # ---------------- roofline of K1 ----------------
+    pairs_rank = sum(m * (m + 1) // 2 for _, m, _ in blocks)
+    flops = pairs_rank * hq * 4 * d
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
+    peak_burst = peaks.get("bf16_tflops", 1590.0)
+    achieved = flops / (k1_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_k1_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except OSError:
+        pass
+
+    # ---------------- e2e through the C-ABI with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        hq_raw = torch.empty(q_raw.shape, dtype=q_raw.dtype, pin_memory=True)
+        hk_raw = torch.empty(k_raw.shape, dtype=k_raw.dtype, pin_memory=True)
+        hv = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+        hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        hq_raw.copy_(q_raw)
+        hk_raw.copy_(k_raw)
+        hv.copy_(v)
+        dq, dk, dv = torch.empty_like(q_raw), torch.empty_like(k_raw), torch.empty_like(v)
+
+        def e2e_step():
+            dq.copy_(hq_raw, non_blocking=True)
+            dk.copy_(hk_raw, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            step(dq, dk, dv, out)
+            hout.copy_(out, non_blocking=True)
+
+        for _ in range(max(1, args.warmup // 2)):
+            e2e_step()
+        barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(1, min(args.steps, 5))
+        x0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        x1.record(stream)
+        barrier()
+        e2e_ms = max_over_ranks(x0.elapsed_time(x1) / n_e2e)
+        e2e = {"value": L / (e2e_ms * 1e-3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int((hq_raw.numel() + hk_raw.numel() + hv.numel()) * 2),
+               "d2h_bytes_per_step": int(hout.numel() * 2), "ms_per_step": e2e_ms,
+               "path": "pinned host Q/K/V -> star_rope/star_phase1_fwd/star_kv_write -> host out"}
+        del hq_raw, hk_raw, hv, hout, dq, dk, dv
+
+    # ---------------- phase-2 decode latency (B=1, one layer) ----------------
+    del q_raw, k_raw, q_rot, out
+    torch.cuda.empty_cache()
+    qd = ops.prng_fill((1, 1, hq, d), seed ^ 4, 1, 1.0, torch.bfloat16, dev)
+    kv_len = torch.tensor([own_rows], dtype=torch.int32, device=dev)
+    gathered_o = torch.empty((world, hq, d), dtype=torch.float32, device=dev)
+    gathered_l = torch.empty((world, hq), dtype=torch.float32, device=dev)
+    ws = ops.Phase2Workspace()
+    k2_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+
+    def decode_step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        o, l = ops.phase2_partial(qd, kpool, vpool, table.view(1, -1), kv_len, own_rows,
+                                  workspace=ws)
+        if ev is not None:
+            ev[1].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered_o, o.view(1, hq, d))
+            dist.all_gather_into_tensor(gathered_l, l.view(1, hq))
+            return ops.merge(gathered_o, gathered_l)
+        return o, l
+
+    n_dec = 50
+    for _ in range(5):
+        decode_step()
+    barrier()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k2_ms_list = []
+    d0.record(stream)
+    for _ in range(n_dec):
+        decode_step()
+    d1.record(stream)
+    barrier()
+    dec_us = max_over_ranks(d0.elapsed_time(d1) / n_dec * 1e3)
+    for _ in range(10):
+        decode_step(k2_ev)
+        barrier()
+        k2_ms_list.append(k2_ev[0].elapsed_time(k2_ev[1]))
+    k2_us = max_over_ranks(float(np.median(k2_ms_list)) * 1e3)
+    kv_bytes = own_rows * hkv * d * 2 * 2
+    decode = {
+        "us_per_token_per_layer": dec_us, "batch": 1, "context": L,
+        "kernel_us": k2_us,
+        "roofline": {"bound": "hbm", "achieved": kv_bytes / (k2_us * 1e-6) / 1e9,
+                     "peak": peaks.get("hbm_gbs", 6532.9), "unit": "GB/s",
+                     "frac": kv_bytes / (k2_us * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6532.9),
+                     "bytes_per_launch": kv_bytes,
+                     "note": "K2 split-KV partial incl. in-GPU split merge; bytes = local KV rows x 8 heads x 128 x 2 (K,V) x 2 B"},
+        "collective": "NCCL all_gather of fp32 (out, lse)" if world > 1 else "none (1 rank)",
+    }
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        t, rows, reps = cpu_sample(budget_s=12.0)
+        cpu = {"value": cpu_tokens_per_s(t, rows), "unit": "tokens/s", "cores": os.cpu_count(),
+               "kind": "port",
+               "sample": f"oracle causal_attention, one q-head x {rows}-row block, {reps} reps "
+                         f"(median {t:.2f} s), extrapolated by score pairs to the cfg2 layer"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (splitmix64 counter fill, reference Prng recipe), random-init shapes",
+        "config": {"workload": "cfg2: Llama-3.1-8B attention, 128K ctx, block 16K, anchor 16K, "
+                               "phase-1 encode of one layer per step",
+                   "context": L, "block": b, "anchor": a, "heads_q": hq, "heads_kv": hkv,
+                   "head_dim": d, "parallelism": f"star{world} (blocks sharded by partition)",
+                   "rank0_blocks": [i for i, _, _ in blocks], "rank0_rows": R,
+                   "l2": "inputs (>= 1.5 GB per rank) exceed the 126 MB L2; no flush needed"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
+                     "frac": achieved / peak_sus, "frac_of_burst_peak": achieved / peak_burst,
+                     "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",
+                     "traffic": traffic, "kernel": "phase1_tc_kernel<128,2>",
+                     "flops_per_launch": flops, "kernel_ms": k1_ms,
+                     "flops_def": "star pairs x Hq x 4 x d (anchor query rows included)"},
+        "decode": decode,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": gpu_launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    args = p.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,160 @@
+/*
+ * star_attn.h — C ABI of the B200 (sm_100a) Star Attention hot path.
+ *
+ * Drop-in boundary for the two-phase attention path of the reference
+ * (`starsim` 0.1.0, /root/reference/pkg/src/starsim, abbreviated ss/).  The
+ * reference has no native code; these entry points replace the numpy compute
+ * sites its Python API funnels into.  Each declaration cites the reference
+ * interface it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no framework types cross the ABI.
+ *  - Device pointers are caller-owned CUDA global memory; the library never
+ *    allocates device memory.  `stream` is a cudaStream_t passed as void*.
+ *  - Every call is stream-ordered and returns STAR_OK or a negative status.
+ *    Status classes mirror the reference's error taxonomy (ss/errors.py:4-17):
+ *      STAR_ESHAPE  -> ShapeError,  STAR_EDOMAIN -> DomainError,
+ *      STAR_ECONFIG -> ConfigError, STAR_ECUDA / STAR_ENOTSUP -> runtime faults.
+ *    star_last_error() returns the message of the last failure on the calling
+ *    thread.
+ *  - Row-major tensors with an explicit row stride (elements) so callers can
+ *    pass slices of fused QKV projections.
+ *  - Log-sum-exp values are natural logs (ln Σ exp), as PartialAttention.lse
+ *    (ss/attention.py:46-64).
+ */
+#ifndef STAR_ATTN_H_
+#define STAR_ATTN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum star_status {
+  STAR_OK = 0,
+  STAR_ESHAPE = -1,
+  STAR_EDOMAIN = -2,
+  STAR_ECONFIG = -3,
+  STAR_ECUDA = -4,
+  STAR_ENOTSUP = -5
+};
+
+enum star_dtype { STAR_F32 = 0, STAR_BF16 = 1 };
+
+/* Library identity and the last error message on this thread. */
+int star_version(void);
+const char* star_last_error(void);
+
+/*
+ * Counter-based splitmix64 fill: out[i] = dtype((2u-1)*scale) with
+ * u = (mix64(seed + (first+i)*0x9E3779B97F4A7C15) >> 11) * 2^-53.
+ * Replaces Prng._block_u64 + prng_fill (ss/numerics.py:217-263); random access,
+ * so the GPU regenerates bit-identical synthetic inputs (first = 1 for a fresh
+ * Prng).
+ */
+int star_prng_fill(void* out, int dtype, int64_t n, uint64_t seed, uint64_t first,
+                   double scale, void* stream);
+
+/*
+ * Rotary embedding on adjacent pairs (2i, 2i+1) at explicit int64 positions:
+ * angle = pos * theta^(-2i/d) reduced in fp64.  x, y: [rows, heads, d] with
+ * row strides; y may alias x.  Replaces rope_apply (ss/numerics.py:161-180) as
+ * called per head by layer_step (ss/toy_model.py:161-162).
+ */
+int star_rope(const void* x, void* y, int dtype, int64_t rows, int heads, int d,
+              int64_t x_row_stride, int64_t y_row_stride, const int64_t* positions,
+              double theta, void* stream);
+
+/*
+ * Phase 1 (K1): causal self-attention over one or more anchor-augmented
+ * blocks concatenated along rows.  Segment s covers rows
+ * [seg_start[s], seg_start[s+1]) of q/k/v/out (seg_start: HOST array of
+ * n_seg+1 offsets); row i of a segment sees keys j <= i of the same segment.
+ * GQA: q head h reads kv head h / (hq/hkv).  q [rows, hq, d], k/v [rows, hkv, d],
+ * out [rows, hq, d] in out_dtype (bf16 or f32), lse fp32 [hq, rows] (nullable).
+ * bf16 uses the tcgen05/TMEM/TMA kernel (d in {64,128}); f32 uses the fp32
+ * check-mode kernel.  Replaces causal_attention (ss/attention.py:109-122) as
+ * driven per (block, layer, head) by _encode_block_channels (ss/sim.py:108-123).
+ */
+int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int n_seg,
+                    const int64_t* seg_start, int hq, int hkv, int d, int64_t q_row_stride,
+                    int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
+                    float* lse, void* stream);
+
+/*
+ * Dense masked attention, one segment: q rows [lq] at absolute offset
+ * q_offset against k/v rows [lk].  mask: 0 = "full", 1 = "causal"
+ * (row i sees keys j <= q_offset + i).  out [lq, hq, d] (dtype of q),
+ * lse fp32 [hq, lq] (nullable).  Rows with no visible key -> STAR_EDOMAIN
+ * (checked on host from the shapes).  Replaces causal_attention /
+ * partial_attention(mask="full"|"causal") (ss/attention.py:109-151).
+ */
+int star_attention_dense(const void* q, const void* k, const void* v, int dtype, int64_t lq,
+                         int64_t lk, int64_t q_offset, int mask, int hq, int hkv, int d,
+                         int64_t q_row_stride, int64_t kv_row_stride, void* out,
+                         int64_t out_row_stride, float* lse, void* stream);
+
+/*
+ * Paged KV cache write: rows [0, n_rows) of k_src/v_src ([n_rows, hkv, d],
+ * row stride src_row_stride) land at logical cache rows
+ * [dst_row0, dst_row0 + n_rows) of one sequence.  Pool layout:
+ * k_pages/v_pages [num_pages, hkv, page_size, d]; logical row r lives in
+ * physical page page_table[r / page_size], slot r % page_size.
+ * Replaces the own-row retention kh[lo:], vh[lo:] (ss/sim.py:117-118,
+ * ss/blocking.py:262-265) and KVCache.append (ss/blocking.py:161-170).
+ */
+int star_kv_write(const void* k_src, const void* v_src, int dtype, int64_t n_rows, int hkv,
+                  int d, int64_t src_row_stride, void* k_pages, void* v_pages,
+                  const int32_t* page_table, int page_size, int64_t dst_row0, void* stream);
+
+/* Inverse of star_kv_write (materialise a sequence's rows densely; for checks). */
+int star_kv_read(const void* k_pages, const void* v_pages, int dtype, const int32_t* page_table,
+                 int page_size, int64_t row0, int64_t n_rows, int hkv, int d, void* k_dst,
+                 void* v_dst, void* stream);
+
+/*
+ * Phase 2 (K2 + intra-GPU split reduction): partial attention of q rows
+ * against each sequence's local paged cache, emitting fp32 (out, lse).
+ * q [batch, lq, hq, d] (dtype q_dtype, contiguous); caches in kv_dtype;
+ * page_table [batch, pages_per_seq] int32; kv_len int32[batch] (device).
+ * own_tail in {0, lq}: when lq, the last lq cache rows are the query's own rows
+ * and q row i sees tail row c only if c <= i (the query host's keep mask,
+ * ss/sim.py:195-200); otherwise every cached row is visible ("full").
+ * out fp32 [batch, lq, hq, d], lse fp32 [batch, lq, hq]; a sequence with
+ * kv_len == 0 yields lse = -inf and out = 0 (the caller skips it, as
+ * _gather_merge skips empty hosts, ss/sim.py:193-194).
+ * n_splits: key-range splits per (sequence, kv head) (0 = auto); the split
+ * partials are merged on device in ascending order.  workspace must hold
+ * star_phase2_workspace_bytes(...) bytes (may be NULL when it returns 0).
+ * Replaces partial_attention(q, K_h, V_h, "full"|keep) (ss/attention.py:125-151)
+ * inside _gather_merge (ss/sim.py:178-213).
+ */
+int64_t star_phase2_workspace_bytes(int batch, int lq, int hq, int d, int n_splits);
+int star_phase2_auto_splits(int batch, int hkv, int64_t max_kv_len, int page_size);
+int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
+                        const void* k_pages, const void* v_pages, int kv_dtype,
+                        const int32_t* page_table, int pages_per_seq, int page_size,
+                        const int32_t* kv_len, int64_t max_kv_len, int own_tail, float* out,
+                        float* lse, int n_splits, void* workspace, void* stream);
+
+/*
+ * K3: log-domain merge of n_parts partials in ascending part order:
+ * s = logaddexp-reduce(lse_p), out = Σ_p exp(lse_p - s) out_p.  outs fp32
+ * [n_parts, rows, d], lses fp32 [n_parts, rows]; parts with lse = -inf are
+ * skipped.  out may be f32 or bf16 (out_dtype).  Replaces merge_partials
+ * (ss/attention.py:154-173).
+ */
+int star_merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d,
+               void* out, int out_dtype, float* lse, void* stream);
+
+/* Debug/validation: C[128x128] fp32 = A[128xK] * B^T via one tcgen05 CTA
+ * (b_mn_major: B given as [K x 128] instead of [128 x K]); K multiple of 64. */
+int star_debug_umma_gemm(const void* a, const void* b, float* c, int K, int b_mn_major,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STAR_ATTN_H_ */

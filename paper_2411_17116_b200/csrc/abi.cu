@@ -1,0 +1,201 @@
+// extern "C" entry points declared in include/star_attn.h: argument checks that
+// mirror the reference's ShapeError / DomainError / ConfigError conditions,
+// then dispatch to the sm_100a kernels.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace star {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+// kernels (defined in the other translation units)
+int prng_fill(void*, int, int64_t, uint64_t, uint64_t, double, cudaStream_t);
+int rope(const void*, void*, int, int64_t, int, int, int64_t, int64_t, const int64_t*, double,
+         cudaStream_t);
+int kv_write(const void*, const void*, int, int64_t, int, int, int64_t, void*, void*,
+             const int32_t*, int, int64_t, cudaStream_t);
+int kv_read(const void*, const void*, int, const int32_t*, int, int64_t, int64_t, int, int, void*,
+            void*, cudaStream_t);
+int attention_simt(const void*, const void*, const void*, int, SegTable&, int, int, int, int64_t,
+                   int64_t, int, void*, int, int64_t, float*, int64_t, cudaStream_t);
+int phase1_tc(const void*, const void*, const void*, SegTable&, int, int, int, int64_t, int64_t,
+              int64_t, void*, int, int64_t, float*, int64_t, cudaStream_t);
+int64_t phase2_workspace_bytes(int, int, int, int, int);
+int phase2_auto_splits(int, int, int64_t, int);
+int phase2_partial(const void*, int, int, int, int, int, int, const void*, const void*, int,
+                   const int32_t*, int, int, const int32_t*, int64_t, int, float*, float*, int,
+                   void*, cudaStream_t);
+int merge(const float*, const float*, int, int64_t, int, void*, int, float*, cudaStream_t);
+int debug_umma_gemm(const void*, const void*, float*, int, int, cudaStream_t);
+
+static int check_heads(int hq, int hkv, int d) {
+  if (hq < 1 || hkv < 1) return fail(STAR_ESHAPE, "head counts must be >= 1 (hq=%d hkv=%d)", hq, hkv);
+  if (hq % hkv) return fail(STAR_ESHAPE, "hq (%d) must be a multiple of hkv (%d)", hq, hkv);
+  if (d < 1) return fail(STAR_ECONFIG, "head_dim must be >= 1, got %d", d);
+  return STAR_OK;
+}
+
+}  // namespace star
+
+using namespace star;
+
+extern "C" {
+
+int star_version(void) { return 1; }
+
+const char* star_last_error(void) { return g_err; }
+
+int star_prng_fill(void* out, int dtype, int64_t n, uint64_t seed, uint64_t first, double scale,
+                   void* stream) {
+  return prng_fill(out, dtype, n, seed, first, scale, (cudaStream_t)stream);
+}
+
+int star_rope(const void* x, void* y, int dtype, int64_t rows, int heads, int d,
+              int64_t x_row_stride, int64_t y_row_stride, const int64_t* positions, double theta,
+              void* stream) {
+  return rope(x, y, dtype, rows, heads, d, x_row_stride, y_row_stride, positions, theta,
+              (cudaStream_t)stream);
+}
+
+int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int n_seg,
+                    const int64_t* seg_start, int hq, int hkv, int d, int64_t q_row_stride,
+                    int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
+                    float* lse, void* stream) {
+  int rc = check_heads(hq, hkv, d);
+  if (out_dtype != STAR_F32 && out_dtype != STAR_BF16)
+    return fail(STAR_ECONFIG, "phase1: unknown out dtype %d", out_dtype);
+  if (rc) return rc;
+  if (n_seg < 0 || n_seg > kMaxSegments)
+    return fail(STAR_ECONFIG, "phase1: %d segments per call (max %d)", n_seg, kMaxSegments);
+  if (n_seg == 0) return STAR_OK;
+  if (seg_start == nullptr) return fail(STAR_ESHAPE, "phase1: seg_start is NULL");
+  if (out == nullptr) return fail(STAR_ESHAPE, "phase1: out is NULL");
+  if (q_row_stride < (int64_t)hq * d || kv_row_stride < (int64_t)hkv * d ||
+      out_row_stride < (int64_t)hq * d)
+    return fail(STAR_ESHAPE, "phase1: row stride smaller than heads*d");
+  SegTable segs;
+  segs.n = n_seg;
+  for (int i = 0; i < n_seg; ++i) {
+    int64_t a = seg_start[i], b = seg_start[i + 1];
+    if (a < 0 || b < a) return fail(STAR_ESHAPE, "phase1: segment %d has bounds [%lld, %lld)", i,
+                                    (long long)a, (long long)b);
+    if (b - a > (1ll << 30)) return fail(STAR_ENOTSUP, "phase1: segment longer than 2^30 rows");
+    segs.q_row0[i] = a;
+    segs.k_row0[i] = a;
+    segs.lq[i] = (int32_t)(b - a);
+    segs.lk[i] = (int32_t)(b - a);
+    segs.q_offset[i] = 0;
+  }
+  const int64_t total = seg_start[n_seg];
+  const int64_t lse_stride = total;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == STAR_BF16 && (d == 64 || d == 128)) {
+    if (total >= (1ll << 31)) return fail(STAR_ENOTSUP, "phase1: more than 2^31 rows per call");
+    return phase1_tc(q, k, v, segs, hq, hkv, d, total, q_row_stride, kv_row_stride, out,
+                     out_dtype == STAR_F32, out_row_stride, lse, lse_stride, s);
+  }
+  return attention_simt(q, k, v, dtype, segs, hq, hkv, d, q_row_stride, kv_row_stride, 1, out,
+                        out_dtype, out_row_stride, lse, lse_stride, s);
+}
+
+int star_attention_dense(const void* q, const void* k, const void* v, int dtype, int64_t lq,
+                         int64_t lk, int64_t q_offset, int mask, int hq, int hkv, int d,
+                         int64_t q_row_stride, int64_t kv_row_stride, void* out,
+                         int64_t out_row_stride, float* lse, void* stream) {
+  int rc = check_heads(hq, hkv, d);
+  if (rc) return rc;
+  if (mask != 0 && mask != 1) return fail(STAR_ECONFIG, "unknown mask kind %d", mask);
+  if (lq < 0 || lk < 0) return fail(STAR_ESHAPE, "negative row counts");
+  if (lq >= (1ll << 31) || lk >= (1ll << 31))
+    return fail(STAR_ENOTSUP, "dense attention: more than 2^31 rows");
+  if (mask == 1 && q_offset + lq > lk)
+    return fail(STAR_ESHAPE, "q rows [%lld, %lld) extend past %lld keys", (long long)q_offset,
+                (long long)(q_offset + lq), (long long)lk);
+  if (lk == 0 && lq > 0) return fail(STAR_EDOMAIN, "partial attention over an empty key set");
+  if (mask == 1 && q_offset < 0) return fail(STAR_EDOMAIN, "q_offset %lld leaves a query row with no keys",
+                                             (long long)q_offset);
+  if (lq == 0) return STAR_OK;
+  SegTable segs;
+  segs.n = 1;
+  segs.q_row0[0] = 0;
+  segs.k_row0[0] = 0;
+  segs.lq[0] = (int32_t)lq;
+  segs.lk[0] = (int32_t)lk;
+  segs.q_offset[0] = (int32_t)q_offset;
+  return attention_simt(q, k, v, dtype, segs, hq, hkv, d, q_row_stride, kv_row_stride, mask, out,
+                        dtype, out_row_stride, lse, lq, (cudaStream_t)stream);
+}
+
+int star_kv_write(const void* k_src, const void* v_src, int dtype, int64_t n_rows, int hkv, int d,
+                  int64_t src_row_stride, void* k_pages, void* v_pages, const int32_t* page_table,
+                  int page_size, int64_t dst_row0, void* stream) {
+  return kv_write(k_src, v_src, dtype, n_rows, hkv, d, src_row_stride, k_pages, v_pages,
+                  page_table, page_size, dst_row0, (cudaStream_t)stream);
+}
+
+int star_kv_read(const void* k_pages, const void* v_pages, int dtype, const int32_t* page_table,
+                 int page_size, int64_t row0, int64_t n_rows, int hkv, int d, void* k_dst,
+                 void* v_dst, void* stream) {
+  return kv_read(k_pages, v_pages, dtype, page_table, page_size, row0, n_rows, hkv, d, k_dst, v_dst,
+                 (cudaStream_t)stream);
+}
+
+int64_t star_phase2_workspace_bytes(int batch, int lq, int hq, int d, int n_splits) {
+  return phase2_workspace_bytes(batch, lq, hq, d, n_splits);
+}
+
+int star_phase2_auto_splits(int batch, int hkv, int64_t max_kv_len, int page_size) {
+  return phase2_auto_splits(batch, hkv, max_kv_len, page_size);
+}
+
+int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
+                        const void* k_pages, const void* v_pages, int kv_dtype,
+                        const int32_t* page_table, int pages_per_seq, int page_size,
+                        const int32_t* kv_len, int64_t max_kv_len, int own_tail, float* out,
+                        float* lse, int n_splits, void* workspace, void* stream) {
+  int rc = check_heads(hq, hkv, d);
+  if (rc) return rc;
+  return phase2_partial(q, q_dtype, batch, lq, hq, hkv, d, k_pages, v_pages, kv_dtype, page_table,
+                        pages_per_seq, page_size, kv_len, max_kv_len, own_tail, out, lse, n_splits,
+                        workspace, (cudaStream_t)stream);
+}
+
+int star_merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d, void* out,
+               int out_dtype, float* lse, void* stream) {
+  return merge(outs, lses, n_parts, rows, d, out, out_dtype, lse, (cudaStream_t)stream);
+}
+
+int star_debug_umma_gemm(const void* a, const void* b, float* c, int K, int b_mn_major,
+                         void* stream) {
+  return debug_umma_gemm(a, b, c, K, b_mn_major, (cudaStream_t)stream);
+}
+
+}  // extern "C"

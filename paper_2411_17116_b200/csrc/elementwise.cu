@@ -1,0 +1,176 @@
+// Elementwise sm_100a kernels of the star-attention path:
+//   * counter-based splitmix64 fill  (ss/numerics.py:183-263)
+//   * adjacent-pair RoPE at explicit positions, fp64 angles (ss/numerics.py:161-180)
+//   * paged KV-cache write / read (own-row retention ss/sim.py:117-118, append
+//     ss/blocking.py:161-170)
+#include "common.cuh"
+
+namespace star {
+
+// ------------------------------------------------------------------ PRNG
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void prng_fill_kernel(T* __restrict__ out, int64_t n, uint64_t seed, uint64_t first,
+                                 double scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = mix64(seed + (first + (uint64_t)i) * 0x9E3779B97F4A7C15ull);
+    double u = (double)(z >> 11) * 0x1.0p-53;
+    // the reference draws at fp32 build precision (prng_fill -> astype(float32));
+    // bf16 inputs are those fp32 values rounded once more to bf16.
+    float f = __double2float_rn((2.0 * u - 1.0) * scale);
+    out[i] = Elem<T>::from_f(f);
+  }
+}
+
+int prng_fill(void* out, int dtype, int64_t n, uint64_t seed, uint64_t first, double scale,
+              cudaStream_t s) {
+  if (n < 0) return fail(STAR_ESHAPE, "prng_fill: negative size %lld", (long long)n);
+  if (!(scale > 0)) return fail(STAR_EDOMAIN, "prng_fill scale must be positive, got %g", scale);
+  if (n == 0) return STAR_OK;
+  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  if (dtype == STAR_F32)
+    prng_fill_kernel<float><<<grid, 256, 0, s>>>((float*)out, n, seed, first, scale);
+  else if (dtype == STAR_BF16)
+    prng_fill_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)out, n, seed, first,
+                                                        scale);
+  else
+    return fail(STAR_ECONFIG, "prng_fill: unknown dtype %d", dtype);
+  STAR_LAUNCH_CHECK("prng_fill");
+  return STAR_OK;
+}
+
+// ------------------------------------------------------------------ RoPE
+// One thread per (row, pair i): the angle pos * theta^(-2i/d) is formed and
+// reduced in fp64 once, then applied to that pair of every head of the row.
+template <typename T>
+__global__ void rope_kernel(const T* __restrict__ x, T* __restrict__ y, int64_t rows, int heads,
+                            int d, int64_t xs, int64_t ys, const int64_t* __restrict__ pos,
+                            double theta) {
+  const int half = d >> 1;
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * half) return;
+  int64_t r = idx / half;
+  int i = (int)(idx - r * half);
+  double inv_freq = pow(theta, -2.0 * (double)i / (double)d);
+  double ang = (double)pos[r] * inv_freq;
+  double sn, cs;
+  sincos(ang, &sn, &cs);
+  const T* xr = x + r * xs + 2 * i;
+  T* yr = y + r * ys + 2 * i;
+  for (int h = 0; h < heads; ++h) {
+    double x0 = (double)Elem<T>::to_f(xr[h * d]);
+    double x1 = (double)Elem<T>::to_f(xr[h * d + 1]);
+    double o0 = x0 * cs - x1 * sn;
+    double o1 = x0 * sn + x1 * cs;
+    yr[h * d] = Elem<T>::from_f(__double2float_rn(o0));
+    yr[h * d + 1] = Elem<T>::from_f(__double2float_rn(o1));
+  }
+}
+
+int rope(const void* x, void* y, int dtype, int64_t rows, int heads, int d, int64_t xs,
+         int64_t ys, const int64_t* pos, double theta, cudaStream_t s) {
+  if (d < 2 || (d & 1)) return fail(STAR_ECONFIG, "rope head_dim must be even and >= 2, got %d", d);
+  if (!(theta > 0)) return fail(STAR_ECONFIG, "rope theta must be positive, got %g", theta);
+  if (rows < 0 || heads < 1) return fail(STAR_ESHAPE, "rope: bad shape rows=%lld heads=%d",
+                                        (long long)rows, heads);
+  if (xs < (int64_t)heads * d || ys < (int64_t)heads * d)
+    return fail(STAR_ESHAPE, "rope: row stride smaller than heads*d");
+  if (rows == 0) return STAR_OK;
+  int64_t n = rows * (d / 2);
+  int grid = (int)((n + 255) / 256);
+  if (dtype == STAR_F32)
+    rope_kernel<float><<<grid, 256, 0, s>>>((const float*)x, (float*)y, rows, heads, d, xs, ys, pos,
+                                            theta);
+  else if (dtype == STAR_BF16)
+    rope_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, (__nv_bfloat16*)y,
+                                                    rows, heads, d, xs, ys, pos, theta);
+  else
+    return fail(STAR_ECONFIG, "rope: unknown dtype %d", dtype);
+  STAR_LAUNCH_CHECK("rope");
+  return STAR_OK;
+}
+
+// ------------------------------------------------------------------ paged KV
+// Vector width W bytes; each thread moves one W-byte chunk of one (row, head).
+template <typename V>
+__global__ void kv_copy_kernel(const char* __restrict__ ks, const char* __restrict__ vs,
+                               char* __restrict__ kp, char* __restrict__ vp,
+                               const int32_t* __restrict__ table, int64_t n_rows, int hkv,
+                               int row_bytes, int64_t src_stride_bytes, int page_size,
+                               int64_t row0, bool to_pages) {
+  const int chunks = row_bytes / (int)sizeof(V);
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = n_rows * hkv * chunks;
+  if (idx >= total) return;
+  int c = (int)(idx % chunks);
+  int64_t t = idx / chunks;
+  int h = (int)(t % hkv);
+  int64_t r = t / hkv;
+  int64_t lr = row0 + r;
+  int64_t page = table[lr / page_size];
+  int slot = (int)(lr % page_size);
+  int64_t poff = ((page * hkv + h) * page_size + slot) * (int64_t)row_bytes + c * sizeof(V);
+  int64_t soff = r * src_stride_bytes + (int64_t)h * row_bytes + c * sizeof(V);
+  if (to_pages) {
+    *reinterpret_cast<V*>(kp + poff) = *reinterpret_cast<const V*>(ks + soff);
+    *reinterpret_cast<V*>(vp + poff) = *reinterpret_cast<const V*>(vs + soff);
+  } else {
+    *reinterpret_cast<V*>(const_cast<char*>(ks) + soff) = *reinterpret_cast<const V*>(kp + poff);
+    *reinterpret_cast<V*>(const_cast<char*>(vs) + soff) = *reinterpret_cast<const V*>(vp + poff);
+  }
+}
+
+static int kv_copy(const void* ks, const void* vs, void* kp, void* vp, int dtype, int64_t n_rows,
+                   int hkv, int d, int64_t src_stride, const int32_t* table, int page_size,
+                   int64_t row0, bool to_pages, cudaStream_t s) {
+  if (dtype != STAR_F32 && dtype != STAR_BF16)
+    return fail(STAR_ECONFIG, "kv copy: unknown dtype %d", dtype);
+  if (n_rows < 0 || hkv < 1 || d < 1 || page_size < 1 || row0 < 0)
+    return fail(STAR_ESHAPE, "kv copy: bad shape");
+  if (src_stride < (int64_t)hkv * d) return fail(STAR_ESHAPE, "kv copy: row stride < hkv*d");
+  if (n_rows == 0) return STAR_OK;
+  int es = dtype == STAR_F32 ? 4 : 2;
+  int row_bytes = d * es;
+  int64_t sb = src_stride * es;
+  bool v16 = (row_bytes % 16 == 0) && (sb % 16 == 0) && ((uintptr_t)ks % 16 == 0) &&
+             ((uintptr_t)vs % 16 == 0);
+  int64_t chunks = v16 ? row_bytes / 16 : (row_bytes % 4 == 0 ? row_bytes / 4 : row_bytes / 2);
+  int64_t total = n_rows * hkv * chunks;
+  int grid = (int)((total + 255) / 256);
+  if (v16)
+    kv_copy_kernel<uint4><<<grid, 256, 0, s>>>((const char*)ks, (const char*)vs, (char*)kp,
+                                               (char*)vp, table, n_rows, hkv, row_bytes, sb,
+                                               page_size, row0, to_pages);
+  else if (row_bytes % 4 == 0)
+    kv_copy_kernel<uint32_t><<<grid, 256, 0, s>>>((const char*)ks, (const char*)vs, (char*)kp,
+                                                  (char*)vp, table, n_rows, hkv, row_bytes, sb,
+                                                  page_size, row0, to_pages);
+  else
+    kv_copy_kernel<uint16_t><<<grid, 256, 0, s>>>((const char*)ks, (const char*)vs, (char*)kp,
+                                                  (char*)vp, table, n_rows, hkv, row_bytes, sb,
+                                                  page_size, row0, to_pages);
+  STAR_LAUNCH_CHECK("kv_copy");
+  return STAR_OK;
+}
+
+int kv_write(const void* k, const void* v, int dtype, int64_t n_rows, int hkv, int d,
+             int64_t src_stride, void* kp, void* vp, const int32_t* table, int page_size,
+             int64_t row0, cudaStream_t s) {
+  return kv_copy(k, v, kp, vp, dtype, n_rows, hkv, d, src_stride, table, page_size, row0, true, s);
+}
+
+int kv_read(const void* kp, const void* vp, int dtype, const int32_t* table, int page_size,
+            int64_t row0, int64_t n_rows, int hkv, int d, void* kd, void* vd, cudaStream_t s) {
+  return kv_copy(kd, vd, const_cast<void*>(kp), const_cast<void*>(vp), dtype, n_rows, hkv, d,
+                 (int64_t)hkv * d, table, page_size, row0, false, s);
+}
+
+}  // namespace star

@@ -1,0 +1,530 @@
+// Phase 1 (K1) on sm_100a tensor cores: causal flash attention over
+// anchor-augmented blocks (segments), bf16 in, fp32 accumulation in TMEM.
+//
+// Reference semantics: causal_attention(q, k, v) per (block, layer, head)
+// (ss/attention.py:109-122) inside _encode_block_channels (ss/sim.py:108-123);
+// the online softmax is the tile-fold of streaming_causal_attention
+// (ss/attention.py:176-210).
+//
+// CTA = one 128-row q tile of one segment for NQ query heads that share a kv
+// head (GQA), so every K/V tile staged by TMA feeds NQ tensor-core pipelines.
+// Warp roles:
+//   warp 0      TMA producer for K tiles (one elected lane)
+//   warp 1      tcgen05.mma issuer (one elected lane)
+//   warp 2      TMEM allocator
+//   warp 3      TMA producer for V tiles
+//   warps 4..   one 128-thread softmax warpgroup per q head: thread = q row =
+//               TMEM lane; S is read with tcgen05.ld, P (bf16) is written to
+//               shared memory in the UMMA K-major SW128 layout, O stays in TMEM
+//               and is rescaled lazily (only when the running max grows by
+//               more than 2^8, exact because numerator and denominator share
+//               the stale max).
+// TMEM columns: S_i at [i*BN, (i+1)*BN), O_i at [NQ*BN + i*D, ...).
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace star {
+
+using namespace sm100;
+
+template <int D, int NQ>
+struct P1Cfg {
+  static constexpr int BM = 128, BN = 128;
+  static constexpr int kSlab = 128 * 128;          // [128 rows x 64 bf16] swizzled slab
+  static constexpr int kSlabs = D / 64;            // slabs per [128 x D] tile
+  static constexpr int kTile = kSlabs * kSlab;     // bytes of a [128 x D] bf16 tile
+  static constexpr int kPTile = 2 * kSlab;         // [128 x 128] bf16 P tile
+  static constexpr int KST = (D == 128) ? 2 : 3;   // K stages
+  static constexpr int VST = (D == 128) ? (NQ == 2 ? 1 : 2) : 2;  // V stages
+  static constexpr int kQOff = 0;
+  static constexpr int kKOff = kQOff + NQ * kTile;
+  static constexpr int kVOff = kKOff + KST * kTile;
+  static constexpr int kPOff = kVOff + VST * kTile;
+  static constexpr int kBarOff = kPOff + NQ * kPTile;
+  static constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 4 * NQ;
+  static constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + align slack
+  static constexpr int kThreads = 128 + 128 * NQ;
+  static constexpr int kTmemCols = (NQ * (BN + D) <= 256) ? 256 : 512;
+  static_assert(NQ * (BN + D) <= 512, "TMEM budget");
+  static_assert(kSmem <= 232448, "shared memory budget");
+};
+
+struct P1Params {
+  SegTable segs;
+  int hq, hkv, d;
+  int64_t out_row_stride;
+  int64_t lse_stride;
+  float scale_log2;
+  void* out;       // bf16 or fp32 rows (out_f32)
+  int out_f32;
+  float* lse;
+};
+
+template <int D, int NQ>
+__global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
+    phase1_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
+                     const __grid_constant__ CUtensorMap tm_k,
+                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ P1Params prm) {
+  using C = P1Cfg<D, NQ>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for SWIZZLE_128B atoms
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + C::KST;
+  uint64_t* v_full = k_empty + C::KST;
+  uint64_t* v_empty = v_full + C::VST;
+  uint64_t* s_full = v_empty + C::VST;
+  uint64_t* s_free = s_full + NQ;
+  uint64_t* p_full = s_free + NQ;
+  uint64_t* o_done = p_full + NQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NQ);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- work item: (segment, q tile) from blockIdx.y (heavy tiles first), head group x ----
+  const int y = blockIdx.y;
+  int s = 0;
+  while (s + 1 < prm.segs.n && prm.segs.tile_start[s + 1] <= y) ++s;
+  const int ntq = prm.segs.tile_start[s + 1] - prm.segs.tile_start[s];
+  const int qt = ntq - 1 - (y - prm.segs.tile_start[s]);
+  const int G = prm.hq / prm.hkv;
+  const int pairs = G / NQ;
+  const int kvh = blockIdx.x / pairs;
+  const int h0 = kvh * G + (blockIdx.x % pairs) * NQ;
+  const int lq = prm.segs.lq[s];
+  const int q_row0 = (int)prm.segs.q_row0[s];
+  const int k_row0 = (int)prm.segs.k_row0[s];
+  const int nkv = qt + 1;  // causal, q and k aligned at row 0 of the segment
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < C::KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
+    for (int i = 0; i < C::VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
+    for (int i = 0; i < NQ; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= K producer =================
+    if (lane == 0) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      mbar_expect_tx(q_full, NQ * C::kTile);
+      for (int i = 0; i < NQ; ++i)
+        for (int a = 0; a < C::kSlabs; ++a)
+          tma_load_3d(smem + C::kQOff + i * C::kTile + a * C::kSlab, &tm_q, q_full, a * 64, h0 + i,
+                      q_row0 + qt * C::BM);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % C::KST;
+        if (j >= C::KST) mbar_wait(&k_empty[st], ((j / C::KST) + 1) & 1);
+        mbar_expect_tx(&k_full[st], C::kTile);
+        for (int a = 0; a < C::kSlabs; ++a)
+          tma_load_3d(smem + C::kKOff + st * C::kTile + a * C::kSlab, &tm_k, &k_full[st], a * 64,
+                      kvh, k_row0 + j * C::BN);
+      }
+    }
+  } else if (warp == 3) {
+    // ================= V producer =================
+    if (lane == 0) {
+      tma_prefetch(&tm_v);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % C::VST;
+        if (j >= C::VST) mbar_wait(&v_empty[st], ((j / C::VST) + 1) & 1);
+        mbar_expect_tx(&v_full[st], C::kTile);
+        for (int a = 0; a < C::kSlabs; ++a)
+          tma_load_3d(smem + C::kVOff + st * C::kTile + a * C::kSlab, &tm_v, &v_full[st], a * 64,
+                      kvh, k_row0 + j * C::BN);
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, C::BN, false, false);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
+      const uint32_t q_addr = smem_u32(smem + C::kQOff);
+      const uint32_t k_addr = smem_u32(smem + C::kKOff);
+      const uint32_t v_addr = smem_u32(smem + C::kVOff);
+      const uint32_t p_addr = smem_u32(smem + C::kPOff);
+      auto issue_s = [&](int j) {
+        const int st = j % C::KST;
+        mbar_wait(&k_full[st], (j / C::KST) & 1);
+        tc_fence_after();
+        for (int i = 0; i < NQ; ++i) {
+          if (j > 0) {
+            mbar_wait(&s_free[i], (j - 1) & 1);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * C::kSlab + (kk & 3) * 32;
+            const uint64_t ad = umma_desc_sw128(q_addr + i * C::kTile + off, 16, 1024);
+            const uint64_t bd = umma_desc_sw128(k_addr + st * C::kTile + off, 16, 1024);
+            umma_bf16_ss(tbase + i * C::BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[i]);
+        }
+        umma_commit(&k_empty[st]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) issue_s(j + 1);
+        const int vs = j % C::VST;
+        mbar_wait(&v_full[vs], (j / C::VST) & 1);
+        for (int i = 0; i < NQ; ++i) {
+          mbar_wait(&p_full[i], j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < C::BN / 16; ++kk) {
+            const uint64_t ad =
+                umma_desc_sw128(p_addr + i * C::kPTile + (kk >> 2) * C::kSlab + (kk & 3) * 32, 16,
+                                1024);
+            const uint64_t bd = umma_desc_sw128(v_addr + vs * C::kTile + kk * 16 * 128, C::kSlab,
+                                                1024);
+            umma_bf16_ss(tbase + NQ * C::BN + i * D, ad, bd, idesc_o,
+                         (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&o_done[i]);
+        }
+        umma_commit(&v_empty[vs]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= softmax warpgroup i =================
+    const int i = (warp - 4) >> 2;
+    const int wq = warp & 3;  // TMEM lane quarter
+    const int r = wq * 32 + lane;
+    const int qrow = qt * C::BM + r;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t s_tm = tbase + lane_off + i * C::BN;
+    const uint32_t o_tm = tbase + lane_off + NQ * C::BN + i * D;
+    unsigned char* p_smem = smem + C::kPOff + i * C::kPTile;
+    const float sl2 = prm.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(&s_full[i], j & 1);
+      tc_fence_after();
+      uint32_t sr[C::BN];
+#pragma unroll
+      for (int c = 0; c < C::BN / 32; ++c)
+        tmem_ld32(s_tm + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[i]);
+
+      float mx = -INFINITY;
+      const int lim = qrow - j * C::BN;  // columns c <= lim are visible
+#pragma unroll
+      for (int c = 0; c < C::BN; ++c) {
+        float v = __uint_as_float(sr[c]) * sl2;
+        if (j == qt && c > lim) v = -INFINITY;
+        sr[c] = __float_as_uint(v);
+        mx = fmaxf(mx, v);
+      }
+      float m_use = m_run, alpha = 1.f;
+      const bool need = (j == 0) || (mx > m_run + 8.f);
+      const bool warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
+      if (j == 0) {
+        m_use = mx;
+      } else if (need) {
+        m_use = mx;
+        alpha = ex2(m_run - mx);
+      }
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < C::BN; ++c) {
+        const float p = ex2(__uint_as_float(sr[c]) - m_use);
+        sr[c] = __float_as_uint(p);
+        rs += p;
+      }
+      if (j > 0) {
+        mbar_wait(&o_done[i], (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (warp_rescale) {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orr[32];
+          tmem_ld32(o_tm + c * 32, orr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+          tmem_st32(o_tm + c * 32, orr);
+        }
+        tmem_wait_st();
+      }
+      l_run = l_run * alpha + rs;
+      m_run = m_use;
+      // P row -> shared memory, K-major SWIZZLE_128B (two 64-column slabs)
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          const int c0 = a * 64 + ch * 8;
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(sr[c0 + 0]), __uint_as_float(sr[c0 + 1]));
+          w.y = pack_bf16x2(__uint_as_float(sr[c0 + 2]), __uint_as_float(sr[c0 + 3]));
+          w.z = pack_bf16x2(__uint_as_float(sr[c0 + 4]), __uint_as_float(sr[c0 + 5]));
+          w.w = pack_bf16x2(__uint_as_float(sr[c0 + 6]), __uint_as_float(sr[c0 + 7]));
+          *reinterpret_cast<uint4*>(p_smem + a * C::kSlab + r * 128 + ((ch ^ (r & 7)) << 4)) = w;
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[i]);
+    }
+    // ---- epilogue: O / l -> bf16 rows; lse = ln(sum) + max ----
+    mbar_wait(&o_done[i], (nkv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l_run;
+    const bool row_ok = qrow < lq && prm.out != nullptr;
+    const int64_t orow_off = (int64_t)(q_row0 + qrow) * prm.out_row_stride + (int64_t)(h0 + i) * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t orr[32];
+      tmem_ld32(o_tm + c * 32, orr);
+      tmem_wait_ld();
+      if (row_ok) {
+        if (prm.out_f32) {
+          float* orow = reinterpret_cast<float*>(prm.out) + orow_off;
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(orow + c * 32 + e) =
+                make_float4(__uint_as_float(orr[e]) * inv, __uint_as_float(orr[e + 1]) * inv,
+                            __uint_as_float(orr[e + 2]) * inv, __uint_as_float(orr[e + 3]) * inv);
+        } else {
+          __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.out) + orow_off;
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(orr[e + 0]) * inv, __uint_as_float(orr[e + 1]) * inv);
+            w.y = pack_bf16x2(__uint_as_float(orr[e + 2]) * inv, __uint_as_float(orr[e + 3]) * inv);
+            w.z = pack_bf16x2(__uint_as_float(orr[e + 4]) * inv, __uint_as_float(orr[e + 5]) * inv);
+            w.w = pack_bf16x2(__uint_as_float(orr[e + 6]) * inv, __uint_as_float(orr[e + 7]) * inv);
+            *reinterpret_cast<uint4*>(orow + c * 32 + e) = w;
+          }
+        }
+      }
+    }
+    if (qrow < lq && prm.lse != nullptr)
+      prm.lse[(int64_t)(h0 + i) * prm.lse_stride + q_row0 + qrow] =
+          (m_run + __log2f(l_run)) * 0.6931471805599453f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_free<C::kTmemCols>(tbase);
+}
+
+// ------------------------------------------------------------------ host
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) ==
+            cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D bf16 map over [rows][heads][d] with row stride (elements); box = 64 x 1 x 128.
+static int make_map_3d(CUtensorMap* map, const void* base, int d, int heads, int64_t rows,
+                       int64_t row_stride) {
+  auto fn = encode_fn();
+  if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if (((uintptr_t)base & 15) || ((row_stride * 2) & 15))
+    return fail(STAR_ESHAPE, "TMA needs 16-byte aligned base and row stride (row_stride=%lld)",
+                (long long)row_stride);
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)heads, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)row_stride * 2};
+  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return STAR_OK;
+}
+
+template <int D, int NQ>
+static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTable& segs, int hq,
+                            int hkv, int64_t total_q_rows, int64_t total_kv_rows, int64_t qs,
+                            int64_t kvs, void* out, int out_f32, int64_t os, float* lse,
+                            int64_t lse_stride, cudaStream_t stream) {
+  using C = P1Cfg<D, NQ>;
+  CUtensorMap tq, tk, tv;
+  int rc;
+  if ((rc = make_map_3d(&tq, q, D, hq, total_q_rows, qs)) != STAR_OK) return rc;
+  if ((rc = make_map_3d(&tk, k, D, hkv, total_kv_rows, kvs)) != STAR_OK) return rc;
+  if ((rc = make_map_3d(&tv, v, D, hkv, total_kv_rows, kvs)) != STAR_OK) return rc;
+  P1Params prm;
+  prm.segs = segs;
+  prm.hq = hq;
+  prm.hkv = hkv;
+  prm.d = D;
+  prm.out_row_stride = os;
+  prm.lse_stride = lse_stride;
+  prm.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
+  prm.out = out;
+  prm.out_f32 = out_f32;
+  prm.lse = lse;
+  prm.segs.tile_start[0] = 0;
+  for (int i = 0; i < segs.n; ++i)
+    prm.segs.tile_start[i + 1] = prm.segs.tile_start[i] + (segs.lq[i] + C::BM - 1) / C::BM;
+  const int tiles = prm.segs.tile_start[segs.n];
+  if (tiles == 0) return STAR_OK;
+  auto kern = phase1_tc_kernel<D, NQ>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  dim3 grid(hkv * (hq / hkv / NQ), tiles);
+  kern<<<grid, C::kThreads, C::kSmem, stream>>>(tq, tk, tv, prm);
+  STAR_LAUNCH_CHECK("phase1_tc");
+  return STAR_OK;
+}
+
+int phase1_tc(const void* q, const void* k, const void* v, SegTable& segs, int hq, int hkv, int d,
+              int64_t total_rows, int64_t qs, int64_t kvs, void* out, int out_f32, int64_t os,
+              float* lse, int64_t lse_stride, cudaStream_t stream) {
+  const int G = hq / hkv;
+  if (d == 128) {
+    if (G % 2 == 0)
+      return launch_phase1_tc<128, 2>(q, k, v, segs, hq, hkv, total_rows, total_rows, qs, kvs, out,
+                                      out_f32, os, lse, lse_stride, stream);
+    return launch_phase1_tc<128, 1>(q, k, v, segs, hq, hkv, total_rows, total_rows, qs, kvs, out,
+                                    out_f32, os, lse, lse_stride, stream);
+  }
+  if (d == 64) {
+    if (G % 2 == 0)
+      return launch_phase1_tc<64, 2>(q, k, v, segs, hq, hkv, total_rows, total_rows, qs, kvs, out,
+                                     out_f32, os, lse, lse_stride, stream);
+    return launch_phase1_tc<64, 1>(q, k, v, segs, hq, hkv, total_rows, total_rows, qs, kvs, out, out_f32, os,
+                                   lse, lse_stride, stream);
+  }
+  return fail(STAR_ENOTSUP, "phase1 tensor-core path needs head_dim 64 or 128, got %d", d);
+}
+
+// ------------------------------------------------------------------ debug GEMM
+// C[128x128] = A[128xK] . B^T, one CTA, one stage per 64-wide K slab.  Used by the
+// tests to pin the UMMA descriptor / TMA swizzle conventions the attention kernel uses.
+__global__ void __launch_bounds__(128, 1)
+    umma_gemm_kernel(const __grid_constant__ CUtensorMap tm_a,
+                     const __grid_constant__ CUtensorMap tm_b, float* c, int K, int b_mn) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* a_s = smem;           // [128 x 64] slab
+  unsigned char* b_s = smem + 16384;   // K-major: [128 x 64]; MN-major: [64 x 128] = 2 slabs of [64 x 64]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 49152);
+  uint64_t* mma_bar = bar + 1;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(mma_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<128>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *slot;
+  for (int kb = 0; kb < K / 64; ++kb) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, 16384 + 16384);
+      tma_load_2d(a_s, &tm_a, bar, kb * 64, 0);
+      if (!b_mn) {
+        tma_load_2d(b_s, &tm_b, bar, kb * 64, 0);
+      } else {
+        // B given as [K][128]: two 64-column MN slabs of 64 K rows each
+        tma_load_2d(b_s, &tm_b, bar, 0, kb * 64);
+        tma_load_2d(b_s + 8192, &tm_b, bar, 64, kb * 64);
+      }
+      mbar_wait(bar, kb & 1);
+      tc_fence_after();
+      const uint32_t idesc = umma_idesc_bf16(128, 128, false, b_mn != 0);
+      for (int kk = 0; kk < 4; ++kk) {
+        uint64_t ad = umma_desc_sw128(smem_u32(a_s) + kk * 32, 16, 1024);
+        uint64_t bd = b_mn ? umma_desc_sw128(smem_u32(b_s) + kk * 16 * 128, 8192, 1024)
+                           : umma_desc_sw128(smem_u32(b_s) + kk * 32, 16, 1024);
+        umma_bf16_ss(tbase, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+      }
+      umma_commit(mma_bar);
+      mbar_wait(mma_bar, kb & 1);
+    }
+    __syncthreads();
+  }
+  tc_fence_after();
+  const int r = warp * 32 + lane;
+  for (int cc = 0; cc < 4; ++cc) {
+    uint32_t v[32];
+    tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + cc * 32, v);
+    tmem_wait_ld();
+    for (int e = 0; e < 32; ++e) c[r * 128 + cc * 32 + e] = __uint_as_float(v[e]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_free<128>(tbase);
+}
+
+int debug_umma_gemm(const void* a, const void* b, float* c, int K, int b_mn, cudaStream_t s) {
+  if (K < 64 || K % 64) return fail(STAR_ESHAPE, "debug gemm: K must be a multiple of 64");
+  auto fn = encode_fn();
+  if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap ta, tb;
+  cuuint32_t estr[2] = {1, 1};
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)K, 128};
+    cuuint64_t str[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {64, 128};
+    if (fn(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a), dims, str, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(STAR_ECUDA, "encode A failed");
+  }
+  {
+    cuuint64_t dims[2];
+    cuuint64_t str[1];
+    cuuint32_t box[2] = {64, (cuuint32_t)(b_mn ? 64 : 128)};
+    if (b_mn) {
+      dims[0] = 128; dims[1] = (cuuint64_t)K; str[0] = 128 * 2;
+    } else {
+      dims[0] = (cuuint64_t)K; dims[1] = 128; str[0] = (cuuint64_t)K * 2;
+    }
+    if (fn(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(b), dims, str, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(STAR_ECUDA, "encode B failed");
+  }
+  int smem = 49152 + 64 + 1024;
+  cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  umma_gemm_kernel<<<1, 128, smem, s>>>(ta, tb, c, K, b_mn);
+  STAR_LAUNCH_CHECK("umma_gemm");
+  return STAR_OK;
+}
+
+}  // namespace star

@@ -1,0 +1,252 @@
+"""Kernel-level operators: torch CUDA tensors in, C-ABI calls out.
+
+Each function validates layouts, passes raw device pointers plus the current
+CUDA stream to libstar_attn.so, and raises the reference's exception classes
+on failure.  No operator has a CPU path: a non-CUDA tensor is an error.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from .errors import ConfigError, DeviceError, ShapeError
+
+_DT = {torch.float32: _lib.STAR_F32, torch.bfloat16: _lib.STAR_BF16}
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise ConfigError(f"unsupported dtype {t.dtype}; use float32 or bfloat16") from None
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise DeviceError("star_attn operators run on CUDA tensors only (no CPU fallback)")
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _rows_view(t: torch.Tensor, name: str) -> tuple[int, int, int]:
+    """[rows, heads, d] with unit inner strides; returns (rows, heads, row_stride)."""
+    if t.dim() != 3:
+        raise ShapeError(f"{name} must be [rows, heads, d], got shape {tuple(t.shape)}")
+    if t.stride(2) != 1 or t.stride(1) != t.shape[2]:
+        raise ShapeError(f"{name} must be contiguous within a row (strides {t.stride()})")
+    return t.shape[0], t.shape[1], t.stride(0)
+
+
+# ---------------------------------------------------------------------------- prng
+def prng_fill(shape, seed: int, first: int = 1, scale: float = 1.0, dtype=torch.float32,
+              device="cuda") -> torch.Tensor:
+    """Draws first..first+n-1 of splitmix64 stream `seed` as (2u-1)*scale (ss/numerics.py:255-263)."""
+    out = torch.empty(shape, dtype=dtype, device=device)
+    _cuda(out)
+    _lib.call("star_prng_fill", out.data_ptr(), dtype_code(out), out.numel(),
+              int(seed) & ((1 << 64) - 1), int(first) & ((1 << 64) - 1), float(scale),
+              _stream(out.device))
+    return out
+
+
+# ---------------------------------------------------------------------------- rope
+def rope(x: torch.Tensor, positions: torch.Tensor, theta: float = 10000.0,
+         out: torch.Tensor | None = None) -> torch.Tensor:
+    """Adjacent-pair RoPE of x [rows, heads, d] at int64 positions [rows] (ss/numerics.py:161-180)."""
+    _cuda(x, positions)
+    rows, heads, xs = _rows_view(x, "x")
+    if out is None:
+        out = torch.empty_like(x)
+    orow, oh, ys = _rows_view(out, "out")
+    if (orow, oh) != (rows, heads) or out.dtype != x.dtype:
+        raise ShapeError("rope out must match x")
+    if positions.dtype != torch.int64 or positions.numel() != rows:
+        raise ShapeError(f"{positions.numel()} positions for {rows} rows (int64 required)")
+    positions = positions.contiguous()
+    _lib.call("star_rope", x.data_ptr(), out.data_ptr(), dtype_code(x), rows, heads, x.shape[2],
+              xs, ys, positions.data_ptr(), float(theta), _stream(x.device))
+    return out
+
+
+# ---------------------------------------------------------------------------- phase 1
+def phase1_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_start: Sequence[int],
+               out: torch.Tensor | None = None, want_lse: bool = False, out_dtype=None):
+    """K1: causal attention of each segment [seg_start[s], seg_start[s+1]) with itself.
+
+    q [rows, hq, d], k/v [rows, hkv, d] (same dtype).  Returns (out, lse|None),
+    lse fp32 [hq, rows] natural log.
+    """
+    _cuda(q, k, v, out)
+    rq, hq, qs = _rows_view(q, "q")
+    rk, hkv, ks = _rows_view(k, "k")
+    rv, hv, vs = _rows_view(v, "v")
+    if (rk, hkv) != (rv, hv) or ks != vs:
+        raise ShapeError("k and v must share shape and row stride")
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ConfigError("q, k, v must share a dtype")
+    d = q.shape[2]
+    if k.shape[2] != d:
+        raise ShapeError(f"q head_dim {d} != k head_dim {k.shape[2]}")
+    seg = [int(x) for x in seg_start]
+    if len(seg) < 1 or seg[-1] > rq or seg[-1] > rk:
+        raise ShapeError("segments extend past the q/k rows")
+    if out is None:
+        out = torch.empty((rq, hq, d), dtype=out_dtype or q.dtype, device=q.device)
+    _, _, os_ = _rows_view(out, "out")
+    lse = torch.empty((hq, seg[-1]), dtype=torch.float32, device=q.device) if want_lse else None
+    arr = (ctypes.c_int64 * len(seg))(*seg)
+    _lib.call("star_phase1_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), dtype_code(q),
+              len(seg) - 1, arr, hq, hkv, d, qs, ks, out.data_ptr(), dtype_code(out), os_,
+              _ptr(lse), _stream(q.device))
+    return out, lse
+
+
+def attention_dense(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_offset: int = 0,
+                    mask: str = "causal", want_lse: bool = True):
+    """Masked attention of q [lq, hq, d] vs k/v [lk, hkv, d]; mask "causal" | "full"."""
+    _cuda(q, k, v)
+    lq, hq, qs = _rows_view(q, "q")
+    lk, hkv, ks = _rows_view(k, "k")
+    if tuple(v.shape) != tuple(k.shape) or v.stride() != k.stride():
+        raise ShapeError("k and v must share shape and strides")
+    if q.shape[2] != k.shape[2]:
+        raise ShapeError(f"q cols {q.shape[2]} != k cols {k.shape[2]}")
+    if mask not in ("causal", "full"):
+        raise ConfigError(f"unknown mask kind {mask!r}")
+    d = q.shape[2]
+    out = torch.empty((lq, hq, d), dtype=q.dtype, device=q.device)
+    lse = torch.empty((hq, lq), dtype=torch.float32, device=q.device) if want_lse else None
+    _lib.call("star_attention_dense", q.data_ptr(), k.data_ptr(), v.data_ptr(), dtype_code(q), lq,
+              lk, int(q_offset), 1 if mask == "causal" else 0, hq, hkv, d, qs, ks,
+              out.data_ptr(), hq * d, _ptr(lse), _stream(q.device))
+    return out, lse
+
+
+# ---------------------------------------------------------------------------- paged KV
+def kv_write(k: torch.Tensor, v: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
+             page_table: torch.Tensor, dst_row0: int) -> None:
+    """Write rows of k/v [n, hkv, d] to logical rows [dst_row0, dst_row0+n) of a paged cache."""
+    _cuda(k, v, k_pages, v_pages, page_table)
+    n, hkv, ks = _rows_view(k, "k")
+    if tuple(v.shape) != tuple(k.shape) or v.stride() != k.stride():
+        raise ShapeError("k and v must share shape and strides")
+    if k_pages.dim() != 4 or k_pages.shape[1] != hkv or k_pages.shape[3] != k.shape[2]:
+        raise ShapeError(f"pool shape {tuple(k_pages.shape)} does not match k {tuple(k.shape)}")
+    if k_pages.dtype != k.dtype:
+        raise ConfigError("pool dtype must match k/v")
+    page_size = k_pages.shape[2]
+    if (dst_row0 + n + page_size - 1) // page_size > page_table.numel():
+        raise ShapeError("page table too short for the written rows")
+    _lib.call("star_kv_write", k.data_ptr(), v.data_ptr(), dtype_code(k), n, hkv, k.shape[2], ks,
+              k_pages.data_ptr(), v_pages.data_ptr(), page_table.data_ptr(), page_size,
+              int(dst_row0), _stream(k.device))
+
+
+def kv_read(k_pages: torch.Tensor, v_pages: torch.Tensor, page_table: torch.Tensor, row0: int,
+            n_rows: int):
+    _cuda(k_pages, v_pages, page_table)
+    _, hkv, page_size, d = k_pages.shape
+    k = torch.empty((n_rows, hkv, d), dtype=k_pages.dtype, device=k_pages.device)
+    v = torch.empty_like(k)
+    _lib.call("star_kv_read", k_pages.data_ptr(), v_pages.data_ptr(), dtype_code(k_pages),
+              page_table.data_ptr(), page_size, int(row0), int(n_rows), hkv, d, k.data_ptr(),
+              v.data_ptr(), _stream(k.device))
+    return k, v
+
+
+# ---------------------------------------------------------------------------- phase 2
+class Phase2Workspace:
+    """Reusable device workspace for the split partials (sized on demand)."""
+
+    def __init__(self):
+        self.buf: torch.Tensor | None = None
+
+    def get(self, nbytes: int, device) -> int | None:
+        if nbytes <= 0:
+            return None
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        return self.buf.data_ptr()
+
+
+_default_ws: dict = {}
+
+
+def phase2_partial(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
+                   page_table: torch.Tensor, kv_len: torch.Tensor, max_kv_len: int,
+                   own_tail: int = 0, n_splits: int = 0, out: torch.Tensor | None = None,
+                   lse: torch.Tensor | None = None, workspace: Phase2Workspace | None = None):
+    """K2: partial attention of q [B, lq, hq, d] vs each sequence's paged cache.
+
+    Returns fp32 (out [B, lq, hq, d], lse [B, lq, hq]).
+    """
+    _cuda(q, k_pages, v_pages, page_table, kv_len)
+    if q.dim() != 4 or not q.is_contiguous():
+        raise ShapeError("q must be a contiguous [batch, lq, hq, d] tensor")
+    B, lq, hq, d = q.shape
+    if k_pages.dim() != 4 or k_pages.shape != v_pages.shape:
+        raise ShapeError("k/v pools must be [num_pages, hkv, page_size, d]")
+    _, hkv, page_size, dk = k_pages.shape
+    if dk != d:
+        raise ShapeError(f"q cols {d} != cache cols {dk}")
+    if page_table.dtype != torch.int32 or kv_len.dtype != torch.int32:
+        raise ConfigError("page_table and kv_len must be int32")
+    if page_table.dim() == 1:
+        page_table = page_table.view(1, -1)
+    if page_table.shape[0] != B or kv_len.numel() != B:
+        raise ShapeError("page_table / kv_len batch mismatch")
+    page_table = page_table.contiguous()
+    pps = page_table.shape[1]
+    if (max_kv_len + page_size - 1) // page_size > pps:
+        raise ShapeError("page table shorter than max_kv_len")
+    lib = _lib.load()
+    if n_splits <= 0:
+        n_splits = lib.star_phase2_auto_splits(B, hkv, int(max_kv_len), page_size)
+    if out is None:
+        out = torch.empty((B, lq, hq, d), dtype=torch.float32, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, lq, hq), dtype=torch.float32, device=q.device)
+    nbytes = lib.star_phase2_workspace_bytes(B, lq, hq, d, n_splits)
+    ws = workspace or _default_ws.setdefault(q.device, Phase2Workspace())
+    _lib.call("star_phase2_partial", q.data_ptr(), dtype_code(q), B, lq, hq, hkv, d,
+              k_pages.data_ptr(), v_pages.data_ptr(), dtype_code(k_pages), page_table.data_ptr(),
+              pps, page_size, kv_len.data_ptr(), int(max_kv_len), int(own_tail), out.data_ptr(),
+              lse.data_ptr(), int(n_splits), ws.get(nbytes, q.device), _stream(q.device))
+    return out, lse
+
+
+def merge(outs: torch.Tensor, lses: torch.Tensor, out_dtype=torch.float32):
+    """K3: merge partials outs [P, rows, d], lses [P, rows] in ascending part order."""
+    _cuda(outs, lses)
+    if outs.dtype != torch.float32 or lses.dtype != torch.float32:
+        raise ConfigError("partials must be fp32")
+    if outs.dim() != 3 or lses.shape != outs.shape[:2]:
+        raise ShapeError("outs [P, rows, d] and lses [P, rows] required")
+    outs, lses = outs.contiguous(), lses.contiguous()
+    P, rows, d = outs.shape
+    out = torch.empty((rows, d), dtype=out_dtype, device=outs.device)
+    lse = torch.empty((rows,), dtype=torch.float32, device=outs.device)
+    _lib.call("star_merge", outs.data_ptr(), lses.data_ptr(), P, rows, d, out.data_ptr(),
+              _DT[out_dtype], lse.data_ptr(), _stream(outs.device))
+    return out, lse
+
+
+def debug_umma_gemm(a: torch.Tensor, b: torch.Tensor, b_mn_major: bool = False) -> torch.Tensor:
+    """C = A . B^T on one tcgen05 CTA (descriptor self-test); a [128, K], b [128, K] or [K, 128]."""
+    _cuda(a, b)
+    K = a.shape[1]
+    c = torch.empty((128, 128), dtype=torch.float32, device=a.device)
+    _lib.call("star_debug_umma_gemm", a.contiguous().data_ptr(), b.contiguous().data_ptr(),
+              c.data_ptr(), K, 1 if b_mn_major else 0, _stream(a.device))
+    return c
