@@ -116,14 +116,16 @@ int star_kv_read(const void* k_pages, const void* v_pages, int dtype, const int3
 /*
  * Phase 2 (K2 + intra-GPU split reduction): partial attention of q rows
  * against each sequence's local paged cache, emitting fp32 (out, lse).
- * q [batch, lq, hq, d] (dtype q_dtype, contiguous); caches in kv_dtype;
- * page_table [batch, pages_per_seq] int32; kv_len int32[batch] (device).
+ * q [batch, lq, hq, d] (dtype q_dtype, contiguous); caches in kv_dtype, pools of
+ * num_pages pages; page_table [batch, pages_per_seq] int32; kv_len int32[batch] (device).
  * own_tail in {0, lq}: when lq, the last lq cache rows are the query's own rows
  * and q row i sees tail row c only if c <= i (the query host's keep mask,
  * ss/sim.py:195-200); otherwise every cached row is visible ("full").
  * out fp32 [batch, lq, hq, d], lse fp32 [batch, lq, hq]; a sequence with
  * kv_len == 0 yields lse = -inf and out = 0 (the caller skips it, as
  * _gather_merge skips empty hosts, ss/sim.py:193-194).
+ * bf16 with d in {64,128} runs the TMA + tensor-core (mma.sync) kernel; f32 runs the
+ * fp32 check-mode kernel.
  * n_splits: key-range splits per (sequence, kv head) (0 = auto); the split
  * partials are merged on device in ascending order.  workspace must hold
  * star_phase2_workspace_bytes(...) bytes (may be NULL when it returns 0).
@@ -133,7 +135,7 @@ int star_kv_read(const void* k_pages, const void* v_pages, int dtype, const int3
 int64_t star_phase2_workspace_bytes(int batch, int lq, int hq, int d, int n_splits);
 int star_phase2_auto_splits(int batch, int hkv, int64_t max_kv_len, int page_size);
 int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
-                        const void* k_pages, const void* v_pages, int kv_dtype,
+                        const void* k_pages, const void* v_pages, int kv_dtype, int64_t num_pages,
                         const int32_t* page_table, int pages_per_seq, int page_size,
                         const int32_t* kv_len, int64_t max_kv_len, int own_tail, float* out,
                         float* lse, int n_splits, void* workspace, void* stream);
@@ -148,10 +150,10 @@ int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, i
 int star_merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d,
                void* out, int out_dtype, float* lse, void* stream);
 
-/* Debug/validation: C[128x128] fp32 = A[128xK] * B^T via one tcgen05 CTA
- * (b_mn_major: B given as [K x 128] instead of [128 x K]); K multiple of 64. */
-int star_debug_umma_gemm(const void* a, const void* b, float* c, int K, int b_mn_major,
-                         void* stream);
+/* Debug/validation: C[128x128] fp32 = A[128xK] * B^T via one tcgen05 CTA.
+ * mode bit 0: B given MN-major as [K x 128]; bit 1: A staged through TMEM.
+ * K multiple of 64. */
+int star_debug_umma_gemm(const void* a, const void* b, float* c, int K, int mode, void* stream);
 
 #ifdef __cplusplus
 }

@@ -38,8 +38,8 @@ SIGNATURES = {
     "star_phase2_workspace_bytes": (c_int64, [c_int, c_int, c_int, c_int, c_int]),
     "star_phase2_auto_splits": (c_int, [c_int, c_int, c_int64, c_int]),
     "star_phase2_partial": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
-                                    c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_int64,
-                                    c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
+                                    c_void_p, c_int, c_int64, c_void_p, c_int, c_int, c_void_p,
+                                    c_int64, c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     "star_merge": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int, c_void_p, c_int, c_void_p,
                            c_void_p]),
     "star_debug_umma_gemm": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),

@@ -51,8 +51,8 @@ int phase1_tc(const void*, const void*, const void*, SegTable&, int, int, int, i
 int64_t phase2_workspace_bytes(int, int, int, int, int);
 int phase2_auto_splits(int, int, int64_t, int);
 int phase2_partial(const void*, int, int, int, int, int, int, const void*, const void*, int,
-                   const int32_t*, int, int, const int32_t*, int64_t, int, float*, float*, int,
-                   void*, cudaStream_t);
+                   int64_t, const int32_t*, int, int, const int32_t*, int64_t, int, float*, float*,
+                   int, void*, cudaStream_t);
 int merge(const float*, const float*, int, int64_t, int, void*, int, float*, cudaStream_t);
 int debug_umma_gemm(const void*, const void*, float*, int, int, cudaStream_t);
 
@@ -177,13 +177,14 @@ int star_phase2_auto_splits(int batch, int hkv, int64_t max_kv_len, int page_siz
 }
 
 int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
-                        const void* k_pages, const void* v_pages, int kv_dtype,
+                        const void* k_pages, const void* v_pages, int kv_dtype, int64_t num_pages,
                         const int32_t* page_table, int pages_per_seq, int page_size,
                         const int32_t* kv_len, int64_t max_kv_len, int own_tail, float* out,
                         float* lse, int n_splits, void* workspace, void* stream) {
   int rc = check_heads(hq, hkv, d);
   if (rc) return rc;
-  return phase2_partial(q, q_dtype, batch, lq, hq, hkv, d, k_pages, v_pages, kv_dtype, page_table,
+  return phase2_partial(q, q_dtype, batch, lq, hq, hkv, d, k_pages, v_pages, kv_dtype, num_pages,
+                        page_table,
                         pages_per_seq, page_size, kv_len, max_kv_len, own_tail, out, lse, n_splits,
                         workspace, (cudaStream_t)stream);
 }
@@ -193,9 +194,8 @@ int star_merge(const float* outs, const float* lses, int n_parts, int64_t rows, 
   return merge(outs, lses, n_parts, rows, d, out, out_dtype, lse, (cudaStream_t)stream);
 }
 
-int star_debug_umma_gemm(const void* a, const void* b, float* c, int K, int b_mn_major,
-                         void* stream) {
-  return debug_umma_gemm(a, b, c, K, b_mn_major, (cudaStream_t)stream);
+int star_debug_umma_gemm(const void* a, const void* b, float* c, int K, int mode, void* stream) {
+  return debug_umma_gemm(a, b, c, K, mode, (cudaStream_t)stream);
 }
 
 }  // extern "C"

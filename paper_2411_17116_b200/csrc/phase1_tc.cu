@@ -9,17 +9,23 @@
 // CTA = one 128-row q tile of one segment for NQ query heads that share a kv
 // head (GQA), so every K/V tile staged by TMA feeds NQ tensor-core pipelines.
 // Warp roles:
-//   warp 0      TMA producer for K tiles (one elected lane)
-//   warp 1      tcgen05.mma issuer (one elected lane)
-//   warp 2      TMEM allocator
-//   warp 3      TMA producer for V tiles
-//   warps 4..   one 128-thread softmax warpgroup per q head: thread = q row =
-//               TMEM lane; S is read with tcgen05.ld, P (bf16) is written to
-//               shared memory in the UMMA K-major SW128 layout, O stays in TMEM
-//               and is rescaled lazily (only when the running max grows by
-//               more than 2^8, exact because numerator and denominator share
-//               the stale max).
-// TMEM columns: S_i at [i*BN, (i+1)*BN), O_i at [NQ*BN + i*D, ...).
+//   warp 0      TMEM allocator; then lane 0 = TMA producer for K tiles and
+//               lane 1 = TMA producer for V tiles (independent pipelines)
+//   warp 1      tcgen05.mma issuer (one lane)
+//   warps 2..   one 128-thread softmax warpgroup per q head: thread = q row =
+//               TMEM lane.  S is read from TMEM in 32-column chunks (pass 1:
+//               row max; pass 2: exp2, row sum, bf16 pack), and P is written
+//               back into TMEM over the S columns already consumed; the P.V
+//               MMA takes its A operand straight from TMEM, so P never touches
+//               shared memory.  O stays in TMEM and is rescaled lazily (only
+//               when the running max grows by more than 2^8 — exact, because
+//               numerator and denominator share the stale max).
+// TMEM columns: S_i / P_i at [i*BN, (i+1)*BN) (P packed bf16x2 in the first BN/2),
+//               O_i at [NQ*BN + i*D, NQ*BN + (i+1)*D).
+// MMA order per kv tile j: for each head i: PV_i(j) then S_i(j+1).  tcgen05.mma
+// executes in issue order, so S_i(j+1) overwriting P_i(j) is safe, and the
+// commit after S_i(j+1) also certifies PV_i(j) (O stable for the rescale).
+
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -35,17 +41,15 @@ struct P1Cfg {
   static constexpr int kSlab = 128 * 128;          // [128 rows x 64 bf16] swizzled slab
   static constexpr int kSlabs = D / 64;            // slabs per [128 x D] tile
   static constexpr int kTile = kSlabs * kSlab;     // bytes of a [128 x D] bf16 tile
-  static constexpr int kPTile = 2 * kSlab;         // [128 x 128] bf16 P tile
-  static constexpr int KST = (D == 128) ? 2 : 3;   // K stages
-  static constexpr int VST = (D == 128) ? (NQ == 2 ? 1 : 2) : 2;  // V stages
+  static constexpr int KST = (D == 128) ? (NQ == 2 ? 2 : 3) : 3;  // K stages
+  static constexpr int VST = (D == 128) ? (NQ == 2 ? 2 : 3) : 3;  // V stages
   static constexpr int kQOff = 0;
   static constexpr int kKOff = kQOff + NQ * kTile;
   static constexpr int kVOff = kKOff + KST * kTile;
-  static constexpr int kPOff = kVOff + VST * kTile;
-  static constexpr int kBarOff = kPOff + NQ * kPTile;
-  static constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 4 * NQ;
+  static constexpr int kBarOff = kVOff + VST * kTile;
+  static constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 3 * NQ;
   static constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + align slack
-  static constexpr int kThreads = 128 + 128 * NQ;
+  static constexpr int kThreads = 64 + 128 * NQ;  // 2 control warps + softmax warpgroups
   static constexpr int kTmemCols = (NQ * (BN + D) <= 256) ? 256 : 512;
   static_assert(NQ * (BN + D) <= 512, "TMEM budget");
   static_assert(kSmem <= 232448, "shared memory budget");
@@ -79,8 +83,7 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
   uint64_t* v_full = k_empty + C::KST;
   uint64_t* v_empty = v_full + C::VST;
   uint64_t* s_full = v_empty + C::VST;
-  uint64_t* s_free = s_full + NQ;
-  uint64_t* p_full = s_free + NQ;
+  uint64_t* p_full = s_full + NQ;
   uint64_t* o_done = p_full + NQ;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NQ);
 
@@ -107,21 +110,20 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
     for (int i = 0; i < C::VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
     for (int i = 0; i < NQ; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
       mbar_init(&p_full[i], 4);
       mbar_init(&o_done[i], 1);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 0) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
   if (warp == 0) {
-    // ================= K producer =================
     if (lane == 0) {
+      // ================= K producer (+ Q once) =================
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_k);
       mbar_expect_tx(q_full, NQ * C::kTile);
@@ -137,10 +139,8 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
           tma_load_3d(smem + C::kKOff + st * C::kTile + a * C::kSlab, &tm_k, &k_full[st], a * 64,
                       kvh, k_row0 + j * C::BN);
       }
-    }
-  } else if (warp == 3) {
-    // ================= V producer =================
-    if (lane == 0) {
+    } else if (lane == 1) {
+      // ================= V producer =================
       tma_prefetch(&tm_v);
       for (int j = 0; j < nkv; ++j) {
         const int st = j % C::VST;
@@ -159,106 +159,111 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       const uint32_t q_addr = smem_u32(smem + C::kQOff);
       const uint32_t k_addr = smem_u32(smem + C::kKOff);
       const uint32_t v_addr = smem_u32(smem + C::kVOff);
-      const uint32_t p_addr = smem_u32(smem + C::kPOff);
-      auto issue_s = [&](int j) {
-        const int st = j % C::KST;
-        mbar_wait(&k_full[st], (j / C::KST) & 1);
-        tc_fence_after();
-        for (int i = 0; i < NQ; ++i) {
-          if (j > 0) {
-            mbar_wait(&s_free[i], (j - 1) & 1);
-            tc_fence_after();
-          }
+      auto issue_s = [&](int i, int st) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * C::kSlab + (kk & 3) * 32;
-            const uint64_t ad = umma_desc_sw128(q_addr + i * C::kTile + off, 16, 1024);
-            const uint64_t bd = umma_desc_sw128(k_addr + st * C::kTile + off, 16, 1024);
-            umma_bf16_ss(tbase + i * C::BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&s_full[i]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kSlab + (kk & 3) * 32;
+          const uint64_t ad = umma_desc_sw128(q_addr + i * C::kTile + off, 16, 1024);
+          const uint64_t bd = umma_desc_sw128(k_addr + st * C::kTile + off, 16, 1024);
+          umma_bf16_ss(tbase + i * C::BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&k_empty[st]);
+        umma_commit(&s_full[i]);
       };
       mbar_wait(q_full, 0);
-      issue_s(0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      for (int i = 0; i < NQ; ++i) issue_s(i, 0);
+      umma_commit(&k_empty[0]);
       for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) issue_s(j + 1);
         const int vs = j % C::VST;
         mbar_wait(&v_full[vs], (j / C::VST) & 1);
+        const bool next = j + 1 < nkv;
+        const int ks = (j + 1) % C::KST;
+        if (next) mbar_wait(&k_full[ks], ((j + 1) / C::KST) & 1);
         for (int i = 0; i < NQ; ++i) {
           mbar_wait(&p_full[i], j & 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < C::BN / 16; ++kk) {
-            const uint64_t ad =
-                umma_desc_sw128(p_addr + i * C::kPTile + (kk >> 2) * C::kSlab + (kk & 3) * 32, 16,
-                                1024);
             const uint64_t bd = umma_desc_sw128(v_addr + vs * C::kTile + kk * 16 * 128, C::kSlab,
                                                 1024);
-            umma_bf16_ss(tbase + NQ * C::BN + i * D, ad, bd, idesc_o,
+            umma_bf16_ts(tbase + NQ * C::BN + i * D, tbase + i * C::BN + kk * 8, bd, idesc_o,
                          (j > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&o_done[i]);
+          if (next) issue_s(i, ks);
         }
         umma_commit(&v_empty[vs]);
+        if (next) umma_commit(&k_empty[ks]);
       }
     }
-  } else if (warp >= 4) {
+  } else {
     // ================= softmax warpgroup i =================
-    const int i = (warp - 4) >> 2;
-    const int wq = warp & 3;  // TMEM lane quarter
+    const int i = (warp - 2) >> 2;
+    const int wq = warp & 3;  // TMEM lane quarter (a warp may only touch lanes 32*(warp%4)..)
     const int r = wq * 32 + lane;
     const int qrow = qt * C::BM + r;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const uint32_t s_tm = tbase + lane_off + i * C::BN;
     const uint32_t o_tm = tbase + lane_off + NQ * C::BN + i * D;
-    unsigned char* p_smem = smem + C::kPOff + i * C::kPTile;
     const float sl2 = prm.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
 
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(&s_full[i], j & 1);
       tc_fence_after();
-      uint32_t sr[C::BN];
+      const bool diag = (j == qt);
+      const int lim = qrow - j * C::BN;  // columns c <= lim are visible on the diagonal tile
+      // ---- pass 1: row max over the scaled scores ----
+      float mx;
+      {
+        uint32_t a[32], b[32];
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < C::BN / 32; ++c)
-        tmem_ld32(s_tm + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[i]);
-
-      float mx = -INFINITY;
-      const int lim = qrow - j * C::BN;  // columns c <= lim are visible
+        for (int half = 0; half < 2; ++half) {
+          tmem_ld32(s_tm + half * 64, a);
+          tmem_ld32(s_tm + half * 64 + 32, b);
+          tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < C::BN; ++c) {
-        float v = __uint_as_float(sr[c]) * sl2;
-        if (j == qt && c > lim) v = -INFINITY;
-        sr[c] = __float_as_uint(v);
-        mx = fmaxf(mx, v);
+          for (int e = 0; e < 32; ++e) {
+            const int c0 = half * 64 + e, c1 = c0 + 32;
+            const float va = (diag && c0 > lim) ? -INFINITY : __uint_as_float(a[e]);
+            const float vb = (diag && c1 > lim) ? -INFINITY : __uint_as_float(b[e]);
+            m4[e & 3] = fmaxf(m4[e & 3], fmaxf(va, vb));
+          }
+        }
+        mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
       }
       float m_use = m_run, alpha = 1.f;
       const bool need = (j == 0) || (mx > m_run + 8.f);
       const bool warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
-      if (j == 0) {
+      if (need) {
+        if (j > 0) alpha = ex2(m_run - mx);
         m_use = mx;
-      } else if (need) {
-        m_use = mx;
-        alpha = ex2(m_run - mx);
       }
-      float rs = 0.f;
+      // ---- pass 2: p = 2^(s*sl2 - m), row sum, bf16 P back into TMEM ----
+      float rsum[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < C::BN; ++c) {
-        const float p = ex2(__uint_as_float(sr[c]) - m_use);
-        sr[c] = __float_as_uint(p);
-        rs += p;
+      for (int c = 0; c < C::BN / 32; ++c) {
+        uint32_t sv[32];
+        tmem_ld32(s_tm + c * 32, sv);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const int col = c * 32 + e;
+          float p0 = ex2(fmaf(__uint_as_float(sv[e]), sl2, -m_use));
+          float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), sl2, -m_use));
+          if (diag && col > lim) p0 = 0.f;
+          if (diag && col + 1 > lim) p1 = 0.f;
+          rsum[(e >> 1) & 3] += p0 + p1;
+          pk[e >> 1] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(s_tm + c * 16, pk);
       }
-      if (j > 0) {
-        mbar_wait(&o_done[i], (j - 1) & 1);
-        tc_fence_after();
-      }
+      const float rs = (rsum[0] + rsum[1]) + (rsum[2] + rsum[3]);
       if (warp_rescale) {
+        // O is stable: s_full(j) was committed after PV(j-1)
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t orr[32];
@@ -268,30 +273,15 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
           for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
           tmem_st32(o_tm + c * 32, orr);
         }
-        tmem_wait_st();
       }
+      tmem_wait_st();
       l_run = l_run * alpha + rs;
       m_run = m_use;
-      // P row -> shared memory, K-major SWIZZLE_128B (two 64-column slabs)
-#pragma unroll
-      for (int a = 0; a < 2; ++a) {
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          const int c0 = a * 64 + ch * 8;
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(sr[c0 + 0]), __uint_as_float(sr[c0 + 1]));
-          w.y = pack_bf16x2(__uint_as_float(sr[c0 + 2]), __uint_as_float(sr[c0 + 3]));
-          w.z = pack_bf16x2(__uint_as_float(sr[c0 + 4]), __uint_as_float(sr[c0 + 5]));
-          w.w = pack_bf16x2(__uint_as_float(sr[c0 + 6]), __uint_as_float(sr[c0 + 7]));
-          *reinterpret_cast<uint4*>(p_smem + a * C::kSlab + r * 128 + ((ch ^ (r & 7)) << 4)) = w;
-        }
-      }
-      fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[i]);
     }
-    // ---- epilogue: O / l -> bf16 rows; lse = ln(sum) + max ----
+    // ---- epilogue: O / l -> rows; lse = ln(sum) + max ----
     mbar_wait(&o_done[i], (nkv - 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l_run;
@@ -330,11 +320,14 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_free<C::kTmemCols>(tbase);
+  if (warp == 0) {
+    __syncwarp();
+    tmem_free<C::kTmemCols>(tbase);
+  }
 }
 
 // ------------------------------------------------------------------ host
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (fn == nullptr) {
     void* p = nullptr;
@@ -350,7 +343,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 3-D bf16 map over [rows][heads][d] with row stride (elements); box = 64 x 1 x 128.
 static int make_map_3d(CUtensorMap* map, const void* base, int d, int heads, int64_t rows,
                        int64_t row_stride) {
-  auto fn = encode_fn();
+  auto fn = tensor_map_encoder();
   if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if (((uintptr_t)base & 15) || ((row_stride * 2) & 15))
     return fail(STAR_ESHAPE, "TMA needs 16-byte aligned base and row stride (row_stride=%lld)",
@@ -429,30 +422,35 @@ int phase1_tc(const void* q, const void* k, const void* v, SegTable& segs, int h
 }
 
 // ------------------------------------------------------------------ debug GEMM
-// C[128x128] = A[128xK] . B^T, one CTA, one stage per 64-wide K slab.  Used by the
-// tests to pin the UMMA descriptor / TMA swizzle conventions the attention kernel uses.
+// C[128x128] = A[128xK] . B^T, one CTA, one stage per 64-wide K slab.  mode bit 0: B given
+// MN-major ([K x 128]); bit 1: A staged into TMEM (the .kind::f16 [a_tmem] form the
+// phase-1 P.V product uses).  Used by the tests to pin the UMMA descriptor / TMA swizzle /
+// TMEM-operand conventions the attention kernel relies on.
 __global__ void __launch_bounds__(128, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tm_a,
-                     const __grid_constant__ CUtensorMap tm_b, float* c, int K, int b_mn) {
+                     const __grid_constant__ CUtensorMap tm_b, float* c, int K, int mode) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* a_s = smem;           // [128 x 64] slab
-  unsigned char* b_s = smem + 16384;   // K-major: [128 x 64]; MN-major: [64 x 128] = 2 slabs of [64 x 64]
+  unsigned char* b_s = smem + 16384;   // K-major: [128 x 64]; MN-major: 2 slabs of [64 x 64]
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 49152);
   uint64_t* mma_bar = bar + 1;
   uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b_mn = mode & 1, a_tm = (mode >> 1) & 1;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     mbar_init(mma_bar, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<128>(slot);
+  if (warp == 0) tmem_alloc<256>(slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *slot;
+  const int r = warp * 32 + lane;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
   for (int kb = 0; kb < K / 64; ++kb) {
     if (threadIdx.x == 0) {
       mbar_expect_tx(bar, 16384 + 16384);
@@ -460,18 +458,39 @@ __global__ void __launch_bounds__(128, 1)
       if (!b_mn) {
         tma_load_2d(b_s, &tm_b, bar, kb * 64, 0);
       } else {
-        // B given as [K][128]: two 64-column MN slabs of 64 K rows each
         tma_load_2d(b_s, &tm_b, bar, 0, kb * 64);
         tma_load_2d(b_s + 8192, &tm_b, bar, 64, kb * 64);
       }
-      mbar_wait(bar, kb & 1);
+    }
+    mbar_wait(bar, kb & 1);
+    if (a_tm) {
+      // row r of the swizzled slab -> 32 packed columns of TMEM lane r
+      uint32_t w[2][16];
+      for (int ch = 0; ch < 8; ++ch) {
+        const uint4 v = *reinterpret_cast<const uint4*>(a_s + r * 128 + ((ch ^ (r & 7)) << 4));
+        w[ch >> 2][(ch & 3) * 4 + 0] = v.x;
+        w[ch >> 2][(ch & 3) * 4 + 1] = v.y;
+        w[ch >> 2][(ch & 3) * 4 + 2] = v.z;
+        w[ch >> 2][(ch & 3) * 4 + 3] = v.w;
+      }
+      tmem_st16(tbase + lane_off + 128, w[0]);
+      tmem_st16(tbase + lane_off + 144, w[1]);
+      tmem_wait_st();
+      tc_fence_before();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
       tc_fence_after();
       const uint32_t idesc = umma_idesc_bf16(128, 128, false, b_mn != 0);
       for (int kk = 0; kk < 4; ++kk) {
-        uint64_t ad = umma_desc_sw128(smem_u32(a_s) + kk * 32, 16, 1024);
         uint64_t bd = b_mn ? umma_desc_sw128(smem_u32(b_s) + kk * 16 * 128, 8192, 1024)
                            : umma_desc_sw128(smem_u32(b_s) + kk * 32, 16, 1024);
-        umma_bf16_ss(tbase, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+        if (a_tm) {
+          umma_bf16_ts(tbase, tbase + 128 + kk * 8, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+        } else {
+          uint64_t ad = umma_desc_sw128(smem_u32(a_s) + kk * 32, 16, 1024);
+          umma_bf16_ss(tbase, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+        }
       }
       umma_commit(mma_bar);
       mbar_wait(mma_bar, kb & 1);
@@ -479,21 +498,21 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
   }
   tc_fence_after();
-  const int r = warp * 32 + lane;
   for (int cc = 0; cc < 4; ++cc) {
     uint32_t v[32];
-    tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + cc * 32, v);
+    tmem_ld32(tbase + lane_off + cc * 32, v);
     tmem_wait_ld();
     for (int e = 0; e < 32; ++e) c[r * 128 + cc * 32 + e] = __uint_as_float(v[e]);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_free<128>(tbase);
+  if (warp == 0) tmem_free<256>(tbase);
 }
 
-int debug_umma_gemm(const void* a, const void* b, float* c, int K, int b_mn, cudaStream_t s) {
+int debug_umma_gemm(const void* a, const void* b, float* c, int K, int mode, cudaStream_t s) {
+  const int b_mn = mode & 1;
   if (K < 64 || K % 64) return fail(STAR_ESHAPE, "debug gemm: K must be a multiple of 64");
-  auto fn = encode_fn();
+  auto fn = tensor_map_encoder();
   if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap ta, tb;
   cuuint32_t estr[2] = {1, 1};
@@ -522,7 +541,7 @@ int debug_umma_gemm(const void* a, const void* b, float* c, int K, int b_mn, cud
   }
   int smem = 49152 + 64 + 1024;
   cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  umma_gemm_kernel<<<1, 128, smem, s>>>(ta, tb, c, K, b_mn);
+  umma_gemm_kernel<<<1, 128, smem, s>>>(ta, tb, c, K, mode);
   STAR_LAUNCH_CHECK("umma_gemm");
   return STAR_OK;
 }

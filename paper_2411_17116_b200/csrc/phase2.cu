@@ -329,8 +329,9 @@ int64_t phase2_workspace_bytes(int batch, int lq, int hq, int d, int n_splits) {
 }
 
 int phase2_auto_splits(int batch, int hkv, int64_t max_kv_len, int page_size) {
-  // aim for >= 2 waves of 2 CTAs/SM, but keep >= 256 keys per split
-  int64_t want = (int64_t)num_sms() * 4 / std::max(1, batch * hkv);
+  // one wave: about one CTA per SM (the bf16 path keeps 128 KB of TMA stages per CTA);
+  // at least 256 keys per split
+  int64_t want = (int64_t)num_sms() / std::max(1, batch * hkv);
   int64_t max_by_len = std::max<int64_t>(1, max_kv_len / 256);
   int64_t s = std::max<int64_t>(1, std::min(want, max_by_len));
   return (int)std::min<int64_t>(s, 1024);
@@ -376,10 +377,16 @@ static int dispatch_qrb(int QR, const void* q, int batch, int lq, int hq, int hk
                                        kv_len, own_tail, chunk, n_splits, out, lse, s);
 }
 
+int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const void* kp,
+               const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
+               const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
+               float* lse, cudaStream_t s);
+
 int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
-                   const void* kp, const void* vp, int kv_dtype, const int32_t* table, int pps,
-                   int page_size, const int32_t* kv_len, int64_t max_kv_len, int own_tail,
-                   float* out, float* lse, int n_splits, void* workspace, cudaStream_t s) {
+                   const void* kp, const void* vp, int kv_dtype, int64_t num_pages,
+                   const int32_t* table, int pps, int page_size, const int32_t* kv_len,
+                   int64_t max_kv_len, int own_tail, float* out, float* lse, int n_splits,
+                   void* workspace, cudaStream_t s) {
   if (batch < 1 || lq < 1 || hq < 1 || hkv < 1 || hq % hkv)
     return fail(STAR_ESHAPE, "phase2: bad heads/batch (batch=%d lq=%d hq=%d hkv=%d)", batch, lq,
                 hq, hkv);
@@ -405,6 +412,15 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
   }
   const int QR = (hq / hkv) * lq;
   int rc;
+  const bool tc_path = kv_dtype == STAR_BF16 && (d == 64 || d == 128) && page_size % 64 == 0 &&
+                       num_pages > 0;
+  if (tc_path) {
+    rc = phase2_mma(q, batch, lq, hq, hkv, d, kp, vp, num_pages, table, pps, page_size, kv_len,
+                    own_tail, chunk, n_splits, po, pl, s);
+    if (rc != STAR_OK) return rc;
+    if (n_splits > 1) return merge(po, pl, n_splits, rows, d, out, STAR_F32, lse, s);
+    return STAR_OK;
+  }
 #define STAR_P2_D(TQ, TKV)                                                                    \
   switch (d) {                                                                                \
     case 128: rc = dispatch_qrb<TQ, TKV, 128>(QR, q, batch, lq, hq, hkv, kp, vp, table, pps,   \

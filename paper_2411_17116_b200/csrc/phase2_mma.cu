@@ -1,0 +1,393 @@
+// Phase 2 (K2), bf16 production path: split-KV partial attention over the paged
+// cache, HBM-bound.  Reference semantics as in phase2.cu (partial_attention /
+// _gather_merge, ss/attention.py:125-151, ss/sim.py:178-213).
+//
+// Design (B200): one CTA streams one key range ("split") of one (sequence, kv
+// head).  A producer warp moves [TN x 64] K/V slabs with TMA (128B swizzle)
+// into a STAGES-deep mbarrier ring; four consumer warps run the two small
+// products on mma.sync m16n8k16 (bf16 in, fp32 accumulate) — the G query heads
+// x lq query rows of the group are packed into the M=16 rows, so one K/V tile
+// load serves every q head of the group.
+//   KEYSPLIT (G*lq <= 16, decode): warp w takes keys [w*TN/4, (w+1)*TN/4) of
+//     each tile with its own online softmax; the 4 warp partials are merged
+//     in shared memory at the end of the split.
+//   row mode (G*lq > 16, query encode): warp w takes q rows [16w, 16w+16) of a
+//     64-row pass over every key of the tile.
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace star {
+
+using namespace sm100;
+
+namespace p2 {
+
+constexpr int TN = 64;       // keys per tile (must divide page_size)
+constexpr int STAGES = 4;
+constexpr int kConsumers = 4;
+constexpr int kThreads = (kConsumers + 1) * 32;
+
+template <int D>
+struct Smem {
+  static constexpr int kSlab = TN * 128;            // [TN rows x 64 bf16] swizzled
+  static constexpr int kTile = (D / 64) * kSlab;    // one K (or V) tile
+  static constexpr int kStage = 2 * kTile;          // K + V
+  static constexpr int kBarOff = STAGES * kStage;
+  static constexpr int kBytes = kBarOff + 2 * STAGES * 8 + 1024;
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// byte address of (row, 16-byte chunk) inside a [rows x 64 bf16] 128B-swizzled slab
+__device__ __forceinline__ uint32_t swz(uint32_t slab, int row, int chunk) {
+  return slab + row * 128 + (((chunk ^ row) & 7) << 4);
+}
+
+}  // namespace p2
+
+template <int D, bool KEYSPLIT>
+__global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
+    const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+    const __nv_bfloat16* __restrict__ q, int lq, int hq, int hkv,
+    const int32_t* __restrict__ page_table, int pages_per_seq, int page_size,
+    const int32_t* __restrict__ kv_len, int own_tail, int64_t chunk, float* __restrict__ out,
+    float* __restrict__ lse, int64_t part_stride_rows, float scale_log2) {
+  using namespace p2;
+  using SM = Smem<D>;
+  constexpr int NT_D = D / 8;  // n-tiles over head dim (P.V output)
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kBarOff);
+  uint64_t* empty = full + STAGES;
+
+  const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  const int G = hq / hkv;
+  const int QR = G * lq;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t len = kv_len[b];
+  const int64_t r0 = (int64_t)split * chunk;
+  const int64_t r1 = min(len, r0 + chunk);
+  const int64_t tail0 = len - own_tail;
+  const int ntiles = r1 > r0 ? (int)((r1 - r0 + TN - 1) / TN) : 0;
+  const int32_t* table = page_table + (int64_t)b * pages_per_seq;
+  float* out_part = out + (int64_t)split * part_stride_rows * D;
+  float* lse_part = lse + (int64_t)split * part_stride_rows;
+  const int n_pass = KEYSPLIT ? 1 : (QR + 63) / 64;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumers) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      int it = 0;
+      for (int pass = 0; pass < n_pass; ++pass) {
+        for (int t = 0; t < ntiles; ++t, ++it) {
+          const int st = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) + 1) & 1);
+          const int64_t row = r0 + (int64_t)t * TN;
+          const int64_t page = table[row / page_size];
+          const int prow = (int)((page * hkv + kvh) * page_size + row % page_size);
+          unsigned char* kb = smem + st * SM::kStage;
+          mbar_expect_tx(&full[st], SM::kStage);
+#pragma unroll
+          for (int a = 0; a < D / 64; ++a) {
+            tma_load_2d(kb + a * SM::kSlab, &tm_k, &full[st], a * 64, prow);
+            tma_load_2d(kb + SM::kTile + a * SM::kSlab, &tm_v, &full[st], a * 64, prow);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ================= consumers =================
+  const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
+  int it = 0;
+  for (int pass = 0; pass < n_pass; ++pass) {
+    const int qbase = KEYSPLIT ? 0 : pass * 64 + warp * 16;  // first q row of this warp
+    // ---- Q A-fragments (16 rows x D) straight from global ----
+    uint32_t qa[D / 16][4];
+    {
+      const int rA = qbase + g4, rB = qbase + g4 + 8;
+      const __nv_bfloat16* qpA = nullptr;
+      const __nv_bfloat16* qpB = nullptr;
+      if (rA < QR) qpA = q + (((int64_t)b * lq + rA / G) * hq + kvh * G + rA % G) * D;
+      if (rB < QR) qpB = q + (((int64_t)b * lq + rB / G) * hq + kvh * G + rB % G) * D;
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        const int c = ks * 16 + t4 * 2;
+        qa[ks][0] = qpA ? *reinterpret_cast<const uint32_t*>(qpA + c) : 0u;
+        qa[ks][1] = qpB ? *reinterpret_cast<const uint32_t*>(qpB + c) : 0u;
+        qa[ks][2] = qpA ? *reinterpret_cast<const uint32_t*>(qpA + c + 8) : 0u;
+        qa[ks][3] = qpB ? *reinterpret_cast<const uint32_t*>(qpB + c + 8) : 0u;
+      }
+    }
+    // query row index (for the own-tail mask) of my two fragment rows
+    const int qiA = (qbase + g4) / G, qiB = (qbase + g4 + 8) / G;
+    float o[NT_D][4];
+#pragma unroll
+    for (int n = 0; n < NT_D; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
+
+    constexpr int KW = KEYSPLIT ? TN / kConsumers : TN;  // keys per warp per tile
+    constexpr int NT_K = KW / 8;                          // n-tiles over keys
+    const int kofs = KEYSPLIT ? warp * KW : 0;
+
+    for (int t = 0; t < ntiles; ++t, ++it) {
+      const int st = it % STAGES;
+      mbar_wait(&full[st], (it / STAGES) & 1);
+      const uint32_t kbase = smem_u32(smem + st * SM::kStage);
+      const uint32_t vbase = kbase + SM::kTile;
+      const int64_t row0 = r0 + (int64_t)t * TN + kofs;
+      if (t == ntiles - 1 && (r1 - r0) % TN != 0) {
+        // rows past the split end may hold stale (even non-finite) data: zero their V rows so
+        // the masked p = 0 never meets a NaN.  Warp w clears tile rows [16w, 16w+16).
+        const int valid = (int)((r1 - r0) % TN);
+        unsigned char* vb = smem + st * SM::kStage + SM::kTile;
+        for (int e = lane; e < 16 * (D / 8); e += 32) {
+          const int rr = warp * 16 + e / (D / 8), chunk = e % (D / 8);
+          if (rr >= valid)
+            *reinterpret_cast<uint4*>(vb + (chunk >> 3) * SM::kSlab + rr * 128 +
+                                      (((chunk ^ rr) & 7) << 4)) = make_uint4(0, 0, 0, 0);
+        }
+        if (KEYSPLIT)
+          __syncwarp();
+        else
+          named_barrier_sync(1, kConsumers * 32);
+      }
+      // ---- S = Q K^T  (16 x KW) ----
+      float sc[NT_K][4];
+#pragma unroll
+      for (int n = 0; n < NT_K; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+#pragma unroll
+      for (int n = 0; n < NT_K; ++n) {
+        const int krow = kofs + n * 8 + (lane & 7);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ks += 2) {
+          // 4 matrices: d chunks 2ks, 2ks+1, 2ks+2, 2ks+3 of keys krow
+          const int chunk = ks * 2 + (lane >> 3);
+          const uint32_t addr = swz(kbase + (chunk >> 3) * SM::kSlab, krow, chunk & 7);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(addr, b0, b1, b2, b3);
+          mma16816(sc[n], qa[ks], b0, b1);
+          mma16816(sc[n], qa[ks + 1], b2, b3);
+        }
+      }
+      // ---- mask + online softmax (rows A = g4, B = g4 + 8) ----
+      float tmA = -INFINITY, tmB = -INFINITY;
+#pragma unroll
+      for (int n = 0; n < NT_K; ++n) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t key = row0 + n * 8 + t4 * 2 + e;
+          bool visA = key < r1, visB = visA;
+          if (own_tail > 0 && key >= tail0) {
+            visA = visA && (key - tail0) <= qiA;
+            visB = visB && (key - tail0) <= qiB;
+          }
+          sc[n][e] = visA ? sc[n][e] * scale_log2 : -INFINITY;
+          sc[n][2 + e] = visB ? sc[n][2 + e] * scale_log2 : -INFINITY;
+          tmA = fmaxf(tmA, sc[n][e]);
+          tmB = fmaxf(tmB, sc[n][2 + e]);
+        }
+      }
+      tmA = fmaxf(tmA, __shfl_xor_sync(0xffffffffu, tmA, 1));
+      tmA = fmaxf(tmA, __shfl_xor_sync(0xffffffffu, tmA, 2));
+      tmB = fmaxf(tmB, __shfl_xor_sync(0xffffffffu, tmB, 1));
+      tmB = fmaxf(tmB, __shfl_xor_sync(0xffffffffu, tmB, 2));
+      const float nA = fmaxf(mA, tmA), nB = fmaxf(mB, tmB);
+      const float aA = (nA == -INFINITY) ? 1.f : ex2(mA - nA);
+      const float aB = (nB == -INFINITY) ? 1.f : ex2(mB - nB);
+      const float uA = (nA == -INFINITY) ? 0.f : nA, uB = (nB == -INFINITY) ? 0.f : nB;
+      float sA = 0.f, sB = 0.f;
+      uint32_t pa[NT_K][2];
+#pragma unroll
+      for (int n = 0; n < NT_K; ++n) {
+        const float p0 = ex2(sc[n][0] - uA), p1 = ex2(sc[n][1] - uA);
+        const float p2v = ex2(sc[n][2] - uB), p3 = ex2(sc[n][3] - uB);
+        sA += p0 + p1;
+        sB += p2v + p3;
+        pa[n][0] = pack_bf16x2(p0, p1);
+        pa[n][1] = pack_bf16x2(p2v, p3);
+      }
+      lA = lA * aA + sA;
+      lB = lB * aB + sB;
+      mA = nA;
+      mB = nB;
+#pragma unroll
+      for (int n = 0; n < NT_D; ++n) {
+        o[n][0] *= aA;
+        o[n][1] *= aA;
+        o[n][2] *= aB;
+        o[n][3] *= aB;
+      }
+      // ---- O += P V  (P: 16 x KW, V: KW x D) ----
+#pragma unroll
+      for (int kk = 0; kk < KW / 16; ++kk) {
+        const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
+        const int vrow = kofs + kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+        for (int nd = 0; nd < NT_D; nd += 2) {
+          // 4 matrices (trans): keys +0/+8 x d chunk nd, nd+1
+          const int chunk = nd + (lane >> 4);
+          const uint32_t addr = swz(vbase + (chunk >> 3) * SM::kSlab, vrow, chunk & 7);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(addr, b0, b1, b2, b3);
+          mma16816(o[nd], a, b0, b1);
+          mma16816(o[nd + 1], a, b2, b3);
+        }
+      }
+      fence_proxy_async_smem();  // generic-proxy zeroing above vs the next TMA write
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    // row sums across the quad
+    lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+    lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+
+    if (KEYSPLIT) {
+      // ---- merge the 4 warp partials in shared memory (stage buffers are idle now) ----
+      float* so = reinterpret_cast<float*>(smem);             // [4][16][D]
+      float* sm = so + kConsumers * 16 * D;                   // [4][16] max
+      float* sl = sm + kConsumers * 16;                       // [4][16] sum
+      named_barrier_sync(1, kConsumers * 32);
+#pragma unroll
+      for (int n = 0; n < NT_D; ++n) {
+        const int c = n * 8 + t4 * 2;
+        so[(warp * 16 + g4) * D + c] = o[n][0];
+        so[(warp * 16 + g4) * D + c + 1] = o[n][1];
+        so[(warp * 16 + g4 + 8) * D + c] = o[n][2];
+        so[(warp * 16 + g4 + 8) * D + c + 1] = o[n][3];
+      }
+      if (t4 == 0) {
+        sm[warp * 16 + g4] = mA;
+        sm[warp * 16 + g4 + 8] = mB;
+        sl[warp * 16 + g4] = lA;
+        sl[warp * 16 + g4 + 8] = lB;
+      }
+      named_barrier_sync(1, kConsumers * 32);
+      for (int e = threadIdx.x; e < QR * D; e += kConsumers * 32) {
+        const int rr = e / D, c = e % D;
+        float m = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kConsumers; ++w) m = fmaxf(m, sm[w * 16 + rr]);
+        float l = 0.f, acc = 0.f;
+        if (m > -INFINITY) {
+#pragma unroll
+          for (int w = 0; w < kConsumers; ++w) {
+            const float f = ex2(sm[w * 16 + rr] - m);
+            l += sl[w * 16 + rr] * f;
+            acc += so[(w * 16 + rr) * D + c] * f;
+          }
+        }
+        const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
+        out_part[orow * D + c] = l > 0.f ? acc / l : 0.f;
+        if (c == 0) lse_part[orow] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+      }
+    } else {
+      // ---- each warp owns its 16 rows ----
+      const int rows[2] = {qbase + g4, qbase + g4 + 8};
+      const float ls[2] = {lA, lB}, ms[2] = {mA, mB};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = rows[h];
+        if (rr >= QR) continue;
+        const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
+        const float inv = ls[h] > 0.f ? 1.f / ls[h] : 0.f;
+#pragma unroll
+        for (int n = 0; n < NT_D; ++n) {
+          const int c = n * 8 + t4 * 2;
+          *reinterpret_cast<float2*>(out_part + orow * D + c) =
+              make_float2(o[n][2 * h] * inv, o[n][2 * h + 1] * inv);
+        }
+        if (t4 == 0)
+          lse_part[orow] = ls[h] > 0.f ? (ms[h] + __log2f(ls[h])) * 0.6931471805599453f : -INFINITY;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+
+int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const void* kp,
+               const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
+               const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
+               float* lse, cudaStream_t s) {
+  using namespace p2;
+  auto fn = tensor_map_encoder();
+  if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if (page_size % TN) return fail(STAR_ECONFIG, "page_size must be a multiple of %d", TN);
+  int64_t rows = num_pages * hkv * page_size;
+  if (rows >= (1ll << 31)) return fail(STAR_ENOTSUP, "KV pool larger than 2^31 rows");
+  CUtensorMap tk, tv;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t str[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)TN};
+  cuuint32_t estr[2] = {1, 1};
+  if (fn(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(kp), dims, str, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+      fn(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(vp), dims, str, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(STAR_ECUDA, "phase2: tensor map encode failed");
+  const int QR = (hq / hkv) * lq;
+  dim3 grid(n_splits, hkv, batch);
+  const float sl2 = (float)(1.4426950408889634 / sqrt((double)d));
+  const int64_t part_rows = (int64_t)batch * lq * hq;
+#define STAR_P2M(DD, KS)                                                                        \
+  do {                                                                                          \
+    auto kern = phase2_mma_kernel<DD, KS>;                                                      \
+    const int bytes = Smem<DD>::kBytes;                                                         \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+    if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \
+    kern<<<grid, kThreads, bytes, s>>>(tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, pps,  \
+                                       page_size, kv_len, own_tail, chunk, out, lse, part_rows, sl2); \
+  } while (0)
+  if (d == 128) {
+    if (QR <= 16) STAR_P2M(128, true); else STAR_P2M(128, false);
+  } else if (d == 64) {
+    if (QR <= 16) STAR_P2M(64, true); else STAR_P2M(64, false);
+  } else {
+    return fail(STAR_ENOTSUP, "phase2 bf16 path needs head_dim 64 or 128");
+  }
+#undef STAR_P2M
+  STAR_LAUNCH_CHECK("phase2_mma");
+  return STAR_OK;
+}
+
+}  // namespace star

@@ -220,7 +220,8 @@ def phase2_partial(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor
     nbytes = lib.star_phase2_workspace_bytes(B, lq, hq, d, n_splits)
     ws = workspace or _default_ws.setdefault(q.device, Phase2Workspace())
     _lib.call("star_phase2_partial", q.data_ptr(), dtype_code(q), B, lq, hq, hkv, d,
-              k_pages.data_ptr(), v_pages.data_ptr(), dtype_code(k_pages), page_table.data_ptr(),
+              k_pages.data_ptr(), v_pages.data_ptr(), dtype_code(k_pages), k_pages.shape[0],
+              page_table.data_ptr(),
               pps, page_size, kv_len.data_ptr(), int(max_kv_len), int(own_tail), out.data_ptr(),
               lse.data_ptr(), int(n_splits), ws.get(nbytes, q.device), _stream(q.device))
     return out, lse
@@ -242,11 +243,12 @@ def merge(outs: torch.Tensor, lses: torch.Tensor, out_dtype=torch.float32):
     return out, lse
 
 
-def debug_umma_gemm(a: torch.Tensor, b: torch.Tensor, b_mn_major: bool = False) -> torch.Tensor:
+def debug_umma_gemm(a: torch.Tensor, b: torch.Tensor, b_mn_major: bool = False,
+                    a_tmem: bool = False) -> torch.Tensor:
     """C = A . B^T on one tcgen05 CTA (descriptor self-test); a [128, K], b [128, K] or [K, 128]."""
     _cuda(a, b)
     K = a.shape[1]
     c = torch.empty((128, 128), dtype=torch.float32, device=a.device)
     _lib.call("star_debug_umma_gemm", a.contiguous().data_ptr(), b.contiguous().data_ptr(),
-              c.data_ptr(), K, 1 if b_mn_major else 0, _stream(a.device))
+              c.data_ptr(), K, (1 if b_mn_major else 0) | (2 if a_tmem else 0), _stream(a.device))
     return c

@@ -37,15 +37,16 @@ def normwise(a, ref):
 
 
 # --------------------------------------------------------------------------- UMMA descriptors
+@pytest.mark.parametrize("a_tmem", [False, True])
 @pytest.mark.parametrize("mn", [False, True])
 @pytest.mark.parametrize("K", [64, 128, 256])
-def test_umma_descriptor_gemm(ops, mn, K):
+def test_umma_descriptor_gemm(ops, mn, K, a_tmem):
     g = torch.Generator(device="cpu").manual_seed(K + mn)
     a = torch.randn(128, K, generator=g).to(torch.bfloat16).cuda()
     b = torch.randn(128, K, generator=g).to(torch.bfloat16).cuda()
     ref = a.float() @ b.float().T
     bb = b.T.contiguous() if mn else b
-    c = ops.debug_umma_gemm(a, bb, b_mn_major=mn)
+    c = ops.debug_umma_gemm(a, bb, b_mn_major=mn, a_tmem=a_tmem)
     torch.cuda.synchronize()
     assert torch.allclose(c, ref, rtol=1e-4, atol=1e-3), float((c - ref).abs().max())
 
