@@ -66,6 +66,61 @@ struct P1Params {
   float* lse;
 };
 
+// Softmax pass 1 over one 128-column S row in TMEM: max of the (masked) raw scores.
+template <bool DIAG>
+__device__ __forceinline__ float row_max(uint32_t s_tm, int lim) {
+  uint32_t a[32], b[32];
+  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    tmem_ld32(s_tm + half * 64, a);
+    tmem_ld32(s_tm + half * 64 + 32, b);
+    tmem_wait_ld();
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float va0 = __uint_as_float(a[e]), va1 = __uint_as_float(a[e + 1]);
+      float vb0 = __uint_as_float(b[e]), vb1 = __uint_as_float(b[e + 1]);
+      if (DIAG) {
+        const int c = half * 64 + e;
+        if (c > lim) va0 = -INFINITY;
+        if (c + 1 > lim) va1 = -INFINITY;
+        if (c + 32 > lim) vb0 = -INFINITY;
+        if (c + 33 > lim) vb1 = -INFINITY;
+      }
+      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(fmaxf(va0, va1), fmaxf(vb0, vb1)));
+    }
+  }
+  return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+}
+
+// Softmax pass 2: p = 2^(s*sl2 - m) per column, row sum, P packed bf16x2 into the TMEM
+// columns of S already consumed (chunk c -> columns [16c, 16c+16)).
+template <bool DIAG>
+__device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, float m) {
+  float rsum[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t sv[32];
+    tmem_ld32(s_tm + c * 32, sv);
+    tmem_wait_ld();
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float p0 = ex2(fmaf(__uint_as_float(sv[e]), sl2, -m));
+      float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), sl2, -m));
+      if (DIAG) {
+        const int col = c * 32 + e;
+        if (col > lim) p0 = 0.f;
+        if (col + 1 > lim) p1 = 0.f;
+      }
+      rsum[(e >> 1) & 3] += p0 + p1;
+      pk[e >> 1] = pack_bf16x2(p0, p1);
+    }
+    tmem_st16(s_tm + c * 16, pk);
+  }
+  return (rsum[0] + rsum[1]) + (rsum[2] + rsum[3]);
+}
+
 template <int D, int NQ>
 __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
     phase1_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
@@ -214,26 +269,12 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       tc_fence_after();
       const bool diag = (j == qt);
       const int lim = qrow - j * C::BN;  // columns c <= lim are visible on the diagonal tile
-      // ---- pass 1: row max over the scaled scores ----
+      // ---- pass 1: row max (raw scores; the scale is applied once to the max) ----
       float mx;
-      {
-        uint32_t a[32], b[32];
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          tmem_ld32(s_tm + half * 64, a);
-          tmem_ld32(s_tm + half * 64 + 32, b);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int c0 = half * 64 + e, c1 = c0 + 32;
-            const float va = (diag && c0 > lim) ? -INFINITY : __uint_as_float(a[e]);
-            const float vb = (diag && c1 > lim) ? -INFINITY : __uint_as_float(b[e]);
-            m4[e & 3] = fmaxf(m4[e & 3], fmaxf(va, vb));
-          }
-        }
-        mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
-      }
+      if (diag)
+        mx = row_max<true>(s_tm, lim) * sl2;
+      else
+        mx = row_max<false>(s_tm, lim) * sl2;
       float m_use = m_run, alpha = 1.f;
       const bool need = (j == 0) || (mx > m_run + 8.f);
       const bool warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
@@ -242,26 +283,8 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
         m_use = mx;
       }
       // ---- pass 2: p = 2^(s*sl2 - m), row sum, bf16 P back into TMEM ----
-      float rsum[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < C::BN / 32; ++c) {
-        uint32_t sv[32];
-        tmem_ld32(s_tm + c * 32, sv);
-        tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int col = c * 32 + e;
-          float p0 = ex2(fmaf(__uint_as_float(sv[e]), sl2, -m_use));
-          float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), sl2, -m_use));
-          if (diag && col > lim) p0 = 0.f;
-          if (diag && col + 1 > lim) p1 = 0.f;
-          rsum[(e >> 1) & 3] += p0 + p1;
-          pk[e >> 1] = pack_bf16x2(p0, p1);
-        }
-        tmem_st16(s_tm + c * 16, pk);
-      }
-      const float rs = (rsum[0] + rsum[1]) + (rsum[2] + rsum[3]);
+      const float rs = diag ? exp_pack<true>(s_tm, lim, sl2, m_use)
+                            : exp_pack<false>(s_tm, lim, sl2, m_use);
       if (warp_rescale) {
         // O is stable: s_full(j) was committed after PV(j-1)
 #pragma unroll

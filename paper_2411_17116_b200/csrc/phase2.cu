@@ -78,6 +78,8 @@ __global__ void __launch_bounds__(kP2Threads, 4) phase2_partial_kernel(
   constexpr int kGroups = QRB * D / 4;         // (q row, 4 head-dim lanes) output groups
   constexpr int kGPT = (kGroups + kP2Threads - 1) / kP2Threads;
   constexpr int kSub = kP2Threads / TN;        // threads per key row in the score phase
+  // XOR swizzle of the 16-byte chunks of a key row, confined to the row (rows of < 8 chunks)
+  constexpr int kSw = kChunks < 8 ? kChunks - 1 : 7;
   static_assert(QRB % kSub == 0, "tile shape");
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* kbuf = smem;                       // [2][TN][row] swizzled 16B chunks
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(kP2Threads, 4) phase2_partial_kernel(
           int64_t page = table[row / page_size];
           int slot = (int)(row % page_size);
           size_t off = (((size_t)page * hkv + kvh) * page_size + slot) * SM::kRowBytes + c * 16;
-          int pc = (c & ~7) | ((c ^ n) & 7);
+          int pc = (c & ~kSw) | ((c ^ n) & kSw);
           cp_async16(kb + n * SM::kRowBytes + pc * 16, reinterpret_cast<const char*>(kpool) + off);
           cp_async16(vb + n * SM::kRowBytes + c * 16, reinterpret_cast<const char*>(vpool) + off);
         } else {
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(kP2Threads, 4) phase2_partial_kernel(
         for (int j = 0; j < QRB / kSub; ++j) sc[j] = 0.f;
 #pragma unroll 2
         for (int c = 0; c < kChunks; ++c) {
-          const int pc = (c & ~7) | ((c ^ n) & 7);
+          const int pc = (c & ~kSw) | ((c ^ n) & kSw);
           uint4 w = *reinterpret_cast<const uint4*>(kb + n * SM::kRowBytes + pc * 16);
           float kf[kPer16];
           VecOf<TKV>::unpack(w, kf);

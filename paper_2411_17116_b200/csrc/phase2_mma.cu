@@ -230,8 +230,10 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
       const float aA = (nA == -INFINITY) ? 1.f : ex2(mA - nA);
       const float aB = (nB == -INFINITY) ? 1.f : ex2(mB - nB);
       const float uA = (nA == -INFINITY) ? 0.f : nA, uB = (nB == -INFINITY) ? 0.f : nB;
+      // P split into bf16 hi + lo parts: the P.V product then carries ~16 mantissa bits of P
+      // (decode is HBM-bound, the extra MMAs are free) instead of bf16's 8.
       float sA = 0.f, sB = 0.f;
-      uint32_t pa[NT_K][2];
+      uint32_t pa[NT_K][2], pl[NT_K][2];
 #pragma unroll
       for (int n = 0; n < NT_K; ++n) {
         const float p0 = ex2(sc[n][0] - uA), p1 = ex2(sc[n][1] - uA);
@@ -240,6 +242,8 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
         sB += p2v + p3;
         pa[n][0] = pack_bf16x2(p0, p1);
         pa[n][1] = pack_bf16x2(p2v, p3);
+        pl[n][0] = pack_bf16x2(p0 - bf16lo(pa[n][0]), p1 - bf16hi(pa[n][0]));
+        pl[n][1] = pack_bf16x2(p2v - bf16lo(pa[n][1]), p3 - bf16hi(pa[n][1]));
       }
       lA = lA * aA + sA;
       lB = lB * aB + sB;
@@ -256,6 +260,7 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
 #pragma unroll
       for (int kk = 0; kk < KW / 16; ++kk) {
         const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
+        const uint32_t al[4] = {pl[2 * kk][0], pl[2 * kk][1], pl[2 * kk + 1][0], pl[2 * kk + 1][1]};
         const int vrow = kofs + kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
 #pragma unroll
         for (int nd = 0; nd < NT_D; nd += 2) {
@@ -266,6 +271,8 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
           ldsm_x4_t(addr, b0, b1, b2, b3);
           mma16816(o[nd], a, b0, b1);
           mma16816(o[nd + 1], a, b2, b3);
+          mma16816(o[nd], al, b0, b1);
+          mma16816(o[nd + 1], al, b2, b3);
         }
       }
       fence_proxy_async_smem();  // generic-proxy zeroing above vs the next TMA write
