@@ -25,7 +25,7 @@ using namespace sm100;
 namespace p2 {
 
 constexpr int TN = 64;       // keys per tile (must divide page_size)
-constexpr int STAGES = 4;
+constexpr int STAGES = 6;
 constexpr int kConsumers = 4;
 constexpr int kThreads = (kConsumers + 1) * 32;
 
@@ -226,9 +226,12 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
       tmA = fmaxf(tmA, __shfl_xor_sync(0xffffffffu, tmA, 2));
       tmB = fmaxf(tmB, __shfl_xor_sync(0xffffffffu, tmB, 1));
       tmB = fmaxf(tmB, __shfl_xor_sync(0xffffffffu, tmB, 2));
-      const float nA = fmaxf(mA, tmA), nB = fmaxf(mB, tmB);
-      const float aA = (nA == -INFINITY) ? 1.f : ex2(mA - nA);
-      const float aB = (nB == -INFINITY) ? 1.f : ex2(mB - nB);
+      // lazy rescale (as in K1): keep the stale max unless the tile max exceeds it by > 2^8;
+      // numerator and denominator share the max, so the result is exact.
+      const bool needA = tmA > mA + 8.f, needB = tmB > mB + 8.f;
+      const float nA = needA ? tmA : mA, nB = needB ? tmB : mB;
+      const float aA = (!needA || mA == -INFINITY) ? 1.f : ex2(mA - nA);
+      const float aB = (!needB || mB == -INFINITY) ? 1.f : ex2(mB - nB);
       const float uA = (nA == -INFINITY) ? 0.f : nA, uB = (nB == -INFINITY) ? 0.f : nB;
       // P split into bf16 hi + lo parts: the P.V product then carries ~16 mantissa bits of P
       // (decode is HBM-bound, the extra MMAs are free) instead of bf16's 8.
@@ -249,12 +252,14 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
       lB = lB * aB + sB;
       mA = nA;
       mB = nB;
+      if (__any_sync(0xffffffffu, needA || needB)) {
 #pragma unroll
-      for (int n = 0; n < NT_D; ++n) {
-        o[n][0] *= aA;
-        o[n][1] *= aA;
-        o[n][2] *= aB;
-        o[n][3] *= aB;
+        for (int n = 0; n < NT_D; ++n) {
+          o[n][0] *= aA;
+          o[n][1] *= aA;
+          o[n][2] *= aB;
+          o[n][3] *= aB;
+        }
       }
       // ---- O += P V  (P: 16 x KW, V: KW x D) ----
 #pragma unroll

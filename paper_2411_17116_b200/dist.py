@@ -1,0 +1,235 @@
+"""Star attention across GPU ranks: one host per rank (torch.distributed + NCCL).
+
+Phase 1 is rank-local: rank r encodes exactly the blocks partition() assigns it
+(ss/blocking.py:68) into its own paged pool; no communication.  Phase 2 per
+layer: every rank runs K2 over its pages, the fp32 (out, lse) partials are
+all-gathered (NCCL over NVLink; 16.5 KB per rank at B = l_q = 1 for Llama-8B
+shapes) and every rank folds them with K3 in ascending rank order — the
+reference's fixed host order (ss/sim.py:189-213).  All-gather rather than
+gather-to-query-host closes the reference's unmetered return path: every rank
+gets the merged attention and can compute layer l+1's queries.
+The ledger records the reference's logical transfers on the query rank.
+
+The collective / merge / ledger helpers are backend-agnostic (any
+torch.distributed backend, an injectable merge function) so the host logic is
+tested with gloo on CPU (tests/test_dist_cpu.py).
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass, field
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from .blocking import AnchorSpec, BlockPlan, PagedKVPool, augment
+from .errors import ConfigError
+from .numerics import Prng, default_dtype
+
+_ANCHOR_SALT = 0xA17C4B10C4ED5EED
+
+
+def init_from_env(backend: str = "nccl") -> tuple[int, int]:
+    """Initialise the default process group from torchrun's env; returns (rank, world)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        if backend == "nccl":
+            local = int(os.environ.get("LOCAL_RANK", "0"))
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return rank, world
+
+
+@dataclass(frozen=True)
+class RankShard:
+    """What one rank owns in phase 1: its blocks (ascending), their own rows and positions."""
+
+    rank: int
+    blocks: tuple[int, ...]
+    seg_start: tuple[int, ...]       # augmented-row offsets of the rank's blocks (segments)
+    own_lo: tuple[int, ...]          # first own row of each block inside the segments
+    cache_row0: tuple[int, ...]      # first cache row of each block in the rank's pool
+    positions: tuple[int, ...]       # position ids of every augmented row, block order
+    cache_positions: tuple[int, ...]  # position ids of the cached (own) rows
+
+    @property
+    def rows(self) -> int:
+        return self.seg_start[-1]
+
+    @property
+    def cache_rows(self) -> int:
+        return len(self.cache_positions)
+
+
+def rank_shard(plan: BlockPlan, blocks_aug, rank: int) -> RankShard:
+    """Host logic of the phase-1 sharding (ss/sim.py:148-174, one host per rank)."""
+    mine = plan.blocks_of(rank)
+    seg, lo, c0, pos, cpos = [0], [], [], [], []
+    for bi in mine:
+        bl = blocks_aug[bi]
+        lo.append(seg[-1] + bl.anchor_prefix_len)
+        c0.append(len(cpos))
+        seg.append(seg[-1] + len(bl.token_ids))
+        pos.extend(bl.position_ids)
+        cpos.extend(bl.own_positions)
+    return RankShard(rank, tuple(mine), tuple(seg), tuple(lo), tuple(c0), tuple(pos), tuple(cpos))
+
+
+def gather_partials(out: torch.Tensor, lse: torch.Tensor, group=None):
+    """All-gather one partial per rank: out [rows, d] fp32, lse [rows] -> [world, rows, d], [world, rows]."""
+    world = dist.get_world_size(group)
+    rows = out.shape[0]
+    outs = torch.empty((world * rows,) + tuple(out.shape[1:]), dtype=out.dtype, device=out.device)
+    lses = torch.empty((world * rows,), dtype=lse.dtype, device=lse.device)
+    dist.all_gather_into_tensor(outs, out.contiguous(), group=group)
+    dist.all_gather_into_tensor(lses, lse.contiguous().view(-1), group=group)
+    return outs.view((world,) + tuple(out.shape)), lses.view(world, rows)
+
+
+def gather_merge(out: torch.Tensor, lse: torch.Tensor, merge_fn: Callable | None = None,
+                 group=None):
+    """All-gather the ranks' partials and fold them in ascending rank order (ranks whose
+    cache is empty contribute lse = -inf and are skipped, ss/sim.py:193-194)."""
+    outs, lses = gather_partials(out, lse, group)
+    if merge_fn is None:
+        from . import ops
+
+        merge_fn = ops.merge
+    return merge_fn(outs, lses)
+
+
+def phase2_ledger_rows(q_rank: int, nonempty_ranks, layers: int, heads: int, l_q: int, d: int):
+    """Ledger rows one phase-2 forward emits, in the reference's order (ss/sim.py:203-210)."""
+    rows = []
+    for _ in range(layers):
+        for _ in range(heads):
+            for r in nonempty_ranks:
+                if r != q_rank:
+                    rows.append((2, r, q_rank, "partial_out", l_q * d))
+                    rows.append((2, r, q_rank, "partial_lse", l_q))
+    return rows
+
+
+@dataclass
+class DistSession:
+    """Per-rank state of a distributed two-phase session."""
+
+    weights: object
+    plan: BlockPlan
+    shard: RankShard
+    pool: PagedKVPool
+    q_rank: int
+    ledger: list = field(default_factory=list)
+    next_position: int = 0
+    last_logits: torch.Tensor | None = None
+    generated: list = field(default_factory=list)
+
+
+def run_phase1_dist(tokens, plan: BlockPlan, spec: AnchorSpec, weights, prng: Prng | None = None,
+                    group=None, page_size: int = 128) -> tuple[RankShard, PagedKVPool]:
+    """Phase 1 on this rank's blocks only (no communication)."""
+    from . import ops
+    from .model import embed, finish_layer, project_qkv
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if world != plan.num_hosts:
+        raise ConfigError(f"plan has {plan.num_hosts} hosts but the group has {world} ranks")
+    cfg = weights.config
+    prng = prng or Prng(cfg.seed ^ _ANCHOR_SALT)
+    blocks = augment(plan, tokens, spec, prng)  # identical on every rank (deterministic)
+    shard = rank_shard(plan, blocks, rank)
+    dev = weights.embedding.device
+    pool = PagedKVPool(cfg.layers, cfg.heads, cfg.head_dim, max(shard.cache_rows, 1), page_size,
+                       default_dtype(), dev)
+    pool.positions.extend(shard.cache_positions)
+    if shard.blocks:
+        x = embed(weights, [t for bi in shard.blocks for t in blocks[bi].token_ids])
+        pos = torch.tensor(shard.positions, dtype=torch.int64, device=dev)
+        for li, lw in enumerate(weights.layers):
+            q, k, v = project_qkv(x, lw, cfg, pos)
+            att, _ = ops.phase1_fwd(q, k, v, list(shard.seg_start), out_dtype=torch.float32)
+            for j, bi in enumerate(shard.blocks):
+                lo, hi = shard.own_lo[j], shard.seg_start[j + 1]
+                pool.write(li, k[lo:hi], v[lo:hi], shard.cache_row0[j])
+            x = finish_layer(x, att, lw)
+    return shard, pool
+
+
+def _phase2_forward_dist(sess: DistSession, token_ids, positions, own_tail: int, group=None):
+    from . import ops
+    from .model import embed, finish_layer, logits_from, project_qkv
+
+    cfg = sess.weights.config
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    x = embed(sess.weights, token_ids)
+    pos = list(positions)
+    H, hd = cfg.heads, cfg.head_dim
+    nonempty = None
+    for li, lw in enumerate(sess.weights.layers):
+        q, k, v = project_qkv(x, lw, cfg, pos)
+        if rank == sess.q_rank:
+            sess.pool.append(li, k, v, pos)
+        l = q.shape[0]
+        n = sess.pool.rows(li)
+        if n:
+            o, s = ops.phase2_partial(q.view(1, l, H, hd).to(sess.pool.dtype).contiguous(),
+                                      sess.pool.k[li], sess.pool.v[li],
+                                      sess.pool.page_table.view(1, -1), sess.pool.kv_len_tensor(li),
+                                      n, own_tail=own_tail if rank == sess.q_rank else 0)
+            o, s = o.view(l * H, hd), s.view(l * H)
+        else:
+            o = torch.zeros((l * H, hd), dtype=torch.float32, device=q.device)
+            s = torch.full((l * H,), float("-inf"), dtype=torch.float32, device=q.device)
+        if nonempty is None:
+            flags = torch.tensor([1 if n else 0], device=q.device)
+            allf = torch.empty(world, dtype=flags.dtype, device=q.device)
+            dist.all_gather_into_tensor(allf, flags, group=group)
+            nonempty = [r for r in range(world) if int(allf[r])]
+        att, _ = gather_merge(o, s, group=group)
+        x = finish_layer(x, att.view(l, H, hd), lw)
+    if rank == sess.q_rank:
+        sess.ledger.extend(phase2_ledger_rows(sess.q_rank, nonempty, cfg.layers, H, len(pos), hd))
+    return logits_from(sess.weights, x)
+
+
+def start_session_dist(weights, tokens, plan: BlockPlan, spec: AnchorSpec, prng=None,
+                       q_rank: int | None = None, group=None):
+    """Distributed start_session (ss/sim.py:284-324): phase 1 per rank, then the query."""
+    world = dist.get_world_size(group)
+    L = plan.context_len
+    tokens = list(tokens)
+    query = tokens[L:]
+    if not query:
+        raise ConfigError("query portion is empty; nothing to encode in phase 2")
+    shard, pool = run_phase1_dist(tokens[:L], plan, spec, weights, prng, group)
+    q_rank = world - 1 if q_rank is None else q_rank
+    sess = DistSession(weights, plan, shard, pool, q_rank)
+    if dist.get_rank(group) == q_rank:
+        sess.ledger += [(2, q_rank, r, "query_broadcast", len(query)) for r in range(world)
+                        if r != q_rank]
+    logits = _phase2_forward_dist(sess, query, range(L, L + len(query)), len(query), group)
+    sess.next_position = L + len(query)
+    sess.last_logits = logits[-1]
+    return logits, sess
+
+
+def decode_dist(sess: DistSession, n_tokens: int, group=None) -> list[int]:
+    """Distributed greedy decode (ss/sim.py:340-368); every rank derives the same token."""
+    world = dist.get_world_size(group)
+    out = []
+    for _ in range(n_tokens):
+        t = int(torch.argmax(sess.last_logits))
+        out.append(t)
+        sess.generated.append(t)
+        if dist.get_rank(group) == sess.q_rank:
+            sess.ledger += [(2, sess.q_rank, r, "query_broadcast", 1) for r in range(world)
+                            if r != sess.q_rank]
+        logits = _phase2_forward_dist(sess, [t], [sess.next_position], 0, group)
+        sess.last_logits = logits[-1]
+        sess.next_position += 1
+    return out

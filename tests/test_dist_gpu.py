@@ -1,0 +1,90 @@
+"""Distributed session (paper_2411_17116_b200.dist) on the B200: 2 ranks share cuda:0.
+
+NCCL refuses two ranks on one device, so the transport here is gloo over CUDA
+tensors; the kernels (K1/K2/K3) are the real ones.  Checked against the
+reference's 2-host golden: identical greedy tokens and ledger, logits within
+the fp32 tolerance of test_model_gpu.
+"""
+
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, port, name, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        import paper_2411_17116_b200 as S
+        from paper_2411_17116_b200 import dist as D
+
+        torch.cuda.set_device(0)
+        torch.backends.cuda.matmul.allow_tf32 = False
+        S.set_default_dtype("float32")
+        g = np.load(os.path.join(GOLDEN, f"model_{name}.npz"))
+        doc = json.loads(str(g["doc"]))
+        md = doc["model"]
+        w = S.init_model(S.ModelConfig(d_model=md["d_model"], heads=md["heads"],
+                                       layers=md["layers"], seed=md["seed"]))
+        plan = S.partition(doc["sequence_len"], doc["block_size"], doc["hosts"])
+        spec = S.AnchorSpec(anchor_len=doc["anchor"]["anchor_len"])
+        toks = list(g["context_tokens"]) + list(g["query_tokens"])
+        logits, sess = D.start_session_dist(w, toks, plan, spec, prng=S.Prng(doc["seed"] ^ 0xA17C4B10C4ED5EED))
+        gen = D.decode_dist(sess, doc["n_generate"])
+        err = float(np.abs(logits.cpu().numpy() - g["query_logits"]).max())
+        csv = None
+        if rank == sess.q_rank:
+            csv = "phase,src,dst,kind,scalar_count\n" + "".join(
+                f"{a},{b},{c},{k},{n}\n" for a, b, c, k, n in sess.ledger)
+        q.put((rank, {"gen": gen, "ref": [int(t) for t in g["generated"]], "err": err, "csv": csv,
+                      "ref_csv": str(g["ledger_csv"]),
+                      "pos": list(sess.pool.positions),
+                      "ref_pos": [int(p) for p in g[f"host{rank}_pos_ch0"]]}))
+    except Exception as e:
+        q.put((rank, {"error": repr(e)}))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["small_n2", "small_n5h2"])
+def test_dist_session_two_ranks(name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in (0, 1):
+        res = out[r]
+        assert "error" not in res, res
+        assert res["gen"] == res["ref"]
+        assert res["err"] < 1e-4
+        assert res["pos"] == res["ref_pos"]
+    assert out[1]["csv"] == out[1]["ref_csv"]
