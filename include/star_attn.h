@@ -127,8 +127,10 @@ int star_kv_read(const void* k_pages, const void* v_pages, int dtype, const int3
  * bf16 with d in {64,128} runs the TMA + tensor-core (mma.sync) kernel; f32 runs the
  * fp32 check-mode kernel.
  * n_splits: key-range splits per (sequence, kv head) (0 = auto); the split
- * partials are merged on device in ascending order.  workspace must hold
- * star_phase2_workspace_bytes(...) bytes (may be NULL when it returns 0).
+ * partials are merged on device in ascending order (bf16: inside the kernel, by the
+ * last CTA of each (sequence, kv head) to finish).  workspace must hold
+ * star_phase2_workspace_bytes(...) bytes (may be NULL when it returns 0) and be
+ * zero-initialised before its first use; calls leave it re-armed for reuse.
  * Replaces partial_attention(q, K_h, V_h, "full"|keep) (ss/attention.py:125-151)
  * inside _gather_merge (ss/sim.py:178-213).
  */

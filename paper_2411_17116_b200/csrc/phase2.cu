@@ -273,35 +273,41 @@ __global__ void __launch_bounds__(kP2Threads, 4) phase2_partial_kernel(
 }
 
 // ------------------------------------------------------------------ K3 merge
-// One warp per output row; weights exp(lse_p - s) and the sum in fp64, as
-// merge_partials does (ss/attention.py:170-173).
+// One warp per output row: the part weights exp(lse_p - s) are formed once per (row, part)
+// (lanes over parts, fp64 like merge_partials, ss/attention.py:170-173) and staged in
+// shared memory; lanes then sweep the head dim, coalesced.
+constexpr int kMergeWarps = 8;
+constexpr int kMergeMaxParts = 512;
+
 template <typename TO>
-__global__ void merge_kernel(const float* __restrict__ outs, const float* __restrict__ lses,
-                             int n_parts, int64_t rows, int d, TO* __restrict__ out,
-                             float* __restrict__ lse) {
-  const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kMergeWarps * 32) merge_kernel(
+    const float* __restrict__ outs, const float* __restrict__ lses, int n_parts, int64_t rows,
+    int d, TO* __restrict__ out, float* __restrict__ lse) {
+  __shared__ float wsm[kMergeWarps][kMergeMaxParts];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * (int64_t)kMergeWarps + warp;
   if (row >= rows) return;
+  float* w = wsm[warp];
   double mx = -INFINITY;
-  for (int p = 0; p < n_parts; ++p) mx = fmax(mx, (double)lses[(int64_t)p * rows + row]);
-  double s = -INFINITY;
-  if (mx > -INFINITY) {
-    double acc = 0.0;
-    for (int p = 0; p < n_parts; ++p) {
-      double l = lses[(int64_t)p * rows + row];
-      if (l > -INFINITY) acc += exp(l - mx);
-    }
-    s = mx + log(acc);
+  for (int p = lane; p < n_parts; p += 32) mx = fmax(mx, (double)lses[(int64_t)p * rows + row]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double acc = 0.0;
+  for (int p = lane; p < n_parts; p += 32) {
+    const double l = lses[(int64_t)p * rows + row];
+    const double e = (l == -INFINITY) ? 0.0 : exp(l - mx);
+    w[p] = (float)e;
+    acc += e;
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  const double s = acc > 0.0 ? mx + log(acc) : -INFINITY;
+  const float inv = acc > 0.0 ? (float)(1.0 / acc) : 0.f;
+  __syncwarp();
   for (int c = lane; c < d; c += 32) {
-    double o = 0.0;
-    if (s > -INFINITY) {
-      for (int p = 0; p < n_parts; ++p) {
-        double l = lses[(int64_t)p * rows + row];
-        if (l > -INFINITY) o += exp(l - s) * (double)outs[((int64_t)p * rows + row) * d + c];
-      }
-    }
-    out[row * d + c] = Elem<TO>::from_f((float)o);
+    float o = 0.f;
+    for (int p = 0; p < n_parts; ++p) o = fmaf(w[p], outs[((int64_t)p * rows + row) * d + c], o);
+    out[row * d + c] = Elem<TO>::from_f(o * inv);
   }
   if (lse != nullptr && lane == 0) lse[row] = (float)s;
 }
@@ -309,13 +315,14 @@ __global__ void merge_kernel(const float* __restrict__ outs, const float* __rest
 int merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d, void* out,
           int out_dtype, float* lse, cudaStream_t s) {
   if (n_parts < 1) return fail(STAR_EDOMAIN, "merge of zero partials");
+  if (n_parts > kMergeMaxParts) return fail(STAR_ENOTSUP, "merge of more than %d partials", kMergeMaxParts);
   if (rows < 0 || d < 1) return fail(STAR_ESHAPE, "merge: bad shape");
   if (rows == 0) return STAR_OK;
-  int grid = (int)((rows + 7) / 8);
+  int grid = (int)((rows + kMergeWarps - 1) / kMergeWarps);
   if (out_dtype == STAR_F32)
-    merge_kernel<float><<<grid, 256, 0, s>>>(outs, lses, n_parts, rows, d, (float*)out, lse);
+    merge_kernel<float><<<grid, kMergeWarps * 32, 0, s>>>(outs, lses, n_parts, rows, d, (float*)out, lse);
   else if (out_dtype == STAR_BF16)
-    merge_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(outs, lses, n_parts, rows, d,
+    merge_kernel<__nv_bfloat16><<<grid, kMergeWarps * 32, 0, s>>>(outs, lses, n_parts, rows, d,
                                                      (__nv_bfloat16*)out, lse);
   else
     return fail(STAR_ECONFIG, "merge: unknown dtype %d", out_dtype);
@@ -324,10 +331,15 @@ int merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d
 }
 
 // ------------------------------------------------------------------ host side
+constexpr int64_t kCounterBytes = 16384;  // 4096 (sequence, kv head) counters
+
 int64_t phase2_workspace_bytes(int batch, int lq, int hq, int d, int n_splits) {
   if (n_splits <= 1) return 0;
   int64_t rows = (int64_t)batch * lq * hq;
-  return (int64_t)n_splits * rows * (d + 1) * 4;
+  // fixed header of int32 arrival counters (one per (sequence, kv head)), then partial
+  // outs + lses; the header sits at the same offset whatever the split count, so a reused
+  // workspace always finds its counters re-armed
+  return kCounterBytes + (int64_t)n_splits * rows * (d + 1) * 4;
 }
 
 int phase2_auto_splits(int batch, int hkv, int64_t max_kv_len, int page_size) {
@@ -336,7 +348,7 @@ int phase2_auto_splits(int batch, int hkv, int64_t max_kv_len, int page_size) {
   int64_t want = (int64_t)num_sms() / std::max(1, batch * hkv);
   int64_t max_by_len = std::max<int64_t>(1, max_kv_len / 256);
   int64_t s = std::max<int64_t>(1, std::min(want, max_by_len));
-  return (int)std::min<int64_t>(s, 1024);
+  return (int)std::min<int64_t>(s, 256);
 }
 
 template <typename TQ, typename TKV, int D, int TN, int QRB>
@@ -382,7 +394,7 @@ static int dispatch_qrb(int QR, const void* q, int batch, int lq, int hq, int hk
 int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const void* kp,
                const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
                const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
-               float* lse, cudaStream_t s);
+               float* lse, float* final_out, float* final_lse, int* counters, cudaStream_t s);
 
 int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
                    const void* kp, const void* vp, int kv_dtype, int64_t num_pages,
@@ -404,12 +416,25 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
   const int TN = kv_dtype == STAR_BF16 ? 64 : 32;
   chunk = (chunk + TN - 1) / TN * TN;
   n_splits = (int)std::max<int64_t>(1, (max_kv_len + chunk - 1) / chunk);
+  if (kv_dtype == STAR_BF16 && n_splits > 1) {
+    // the in-kernel split fix-up stages n_splits x QR weights in the idle TMA ring
+    const int64_t qr = (int64_t)(hq / hkv) * lq;
+    const int64_t cap = ((d == 128 ? 6 * 32768 : 6 * 16384) - 64) / (4 * qr) - 1;
+    if (n_splits > cap) {
+      n_splits = (int)std::max<int64_t>(1, cap);
+      chunk = (max_kv_len + n_splits - 1) / n_splits;
+      chunk = (chunk + TN - 1) / TN * TN;
+      n_splits = (int)std::max<int64_t>(1, (max_kv_len + chunk - 1) / chunk);
+    }
+  }
   float* po = out;
   float* pl = lse;
   int64_t rows = (int64_t)batch * lq * hq;
   if (n_splits > 1) {
     if (workspace == nullptr) return fail(STAR_ECONFIG, "phase2: workspace required for splits");
-    po = reinterpret_cast<float*>(workspace);
+    if ((int64_t)batch * hkv * 4 > kCounterBytes)
+      return fail(STAR_ENOTSUP, "phase2: batch x kv heads > %lld", (long long)(kCounterBytes / 4));
+    po = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + kCounterBytes);
     pl = po + (int64_t)n_splits * rows * d;
   }
   const int QR = (hq / hkv) * lq;
@@ -417,11 +442,11 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
   const bool tc_path = kv_dtype == STAR_BF16 && (d == 64 || d == 128) && page_size % 64 == 0 &&
                        num_pages > 0;
   if (tc_path) {
-    rc = phase2_mma(q, batch, lq, hq, hkv, d, kp, vp, num_pages, table, pps, page_size, kv_len,
-                    own_tail, chunk, n_splits, po, pl, s);
-    if (rc != STAR_OK) return rc;
-    if (n_splits > 1) return merge(po, pl, n_splits, rows, d, out, STAR_F32, lse, s);
-    return STAR_OK;
+    // split partials are folded inside the kernel by the last CTA of each (sequence, kv
+    // head); the arrival counters live after the partials in the (zero-initialised) workspace
+    int* counters = n_splits > 1 ? reinterpret_cast<int*>(workspace) : nullptr;
+    return phase2_mma(q, batch, lq, hq, hkv, d, kp, vp, num_pages, table, pps, page_size, kv_len,
+                      own_tail, chunk, n_splits, po, pl, out, lse, counters, s);
   }
 #define STAR_P2_D(TQ, TKV)                                                                    \
   switch (d) {                                                                                \

@@ -66,13 +66,73 @@ __device__ __forceinline__ uint32_t swz(uint32_t slab, int row, int chunk) {
 
 }  // namespace p2
 
+// Serial split-K fix-up: the last CTA of a (sequence, kv head) to finish folds the
+// gridDim.x split partials (still L2-resident) with the merge rule, in ascending split
+// order, and re-arms the counter.  Consumer threads only (128; the producer has exited).
+template <int D>
+__device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq, int G,
+                            const float* ws_out, const float* ws_lse, int64_t part_rows,
+                            float* final_out, float* final_lse, int* counters) {
+  using namespace p2;
+  constexpr int NT = kConsumers * 32;
+  const int tid = threadIdx.x;
+  const int nsp = gridDim.x;
+  const int QR = G * lq;
+  int* flag = reinterpret_cast<int*>(smem);
+  __threadfence();
+  named_barrier_sync(1, NT);
+  if (tid == 0) {
+    const int old = atomicAdd(&counters[b * gridDim.y + kvh], 1);
+    *flag = (old == nsp - 1);
+  }
+  named_barrier_sync(1, NT);
+  if (!*flag) return;
+  __threadfence();
+  float* w = reinterpret_cast<float*>(smem + 16);  // [nsp][QR] weights
+  float* srow = w + nsp * QR;                       // [QR] merged lse
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int rr = warp; rr < QR; rr += NT / 32) {
+    const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
+    float m = -INFINITY;
+    for (int p = lane; p < nsp; p += 32) m = fmaxf(m, ws_lse[p * part_rows + orow]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float acc = 0.f;
+    for (int p = lane; p < nsp; p += 32) {
+      const float l = ws_lse[p * part_rows + orow];
+      const float e = (l == -INFINITY) ? 0.f : __expf(l - m);
+      w[p * QR + rr] = e;
+      acc += e;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const float inv = acc > 0.f ? 1.f / acc : 0.f;
+    for (int p = lane; p < nsp; p += 32) w[p * QR + rr] *= inv;
+    if (lane == 0) {
+      const float sl = acc > 0.f ? m + __logf(acc) : -INFINITY;
+      srow[rr] = sl;
+      final_lse[orow] = sl;
+    }
+  }
+  named_barrier_sync(1, NT);
+  for (int e = tid; e < QR * D; e += NT) {
+    const int rr = e / D, c = e % D;
+    const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
+    float acc = 0.f;
+    for (int p = 0; p < nsp; ++p) acc = fmaf(w[p * QR + rr], ws_out[(p * part_rows + orow) * D + c], acc);
+    final_out[orow * D + c] = acc;
+  }
+  if (tid == 0) counters[b * gridDim.y + kvh] = 0;  // re-arm for the next launch
+}
+
 template <int D, bool KEYSPLIT>
 __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
     const __nv_bfloat16* __restrict__ q, int lq, int hq, int hkv,
     const int32_t* __restrict__ page_table, int pages_per_seq, int page_size,
     const int32_t* __restrict__ kv_len, int own_tail, int64_t chunk, float* __restrict__ out,
-    float* __restrict__ lse, int64_t part_stride_rows, float scale_log2) {
+    float* __restrict__ lse, int64_t part_stride_rows, float scale_log2,
+    float* __restrict__ final_out, float* __restrict__ final_lse, int* __restrict__ counters) {
   using namespace p2;
   using SM = Smem<D>;
   constexpr int NT_D = D / 8;  // n-tiles over head dim (P.V output)
@@ -350,6 +410,8 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
       }
     }
   }
+  if (gridDim.x > 1) split_fixup<D>(smem, b, kvh, lq, hq, G, out, lse, part_stride_rows, final_out,
+                                    final_lse, counters);
 }
 
 // ------------------------------------------------------------------ host
@@ -358,7 +420,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const void* kp,
                const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
                const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
-               float* lse, cudaStream_t s) {
+               float* lse, float* final_out, float* final_lse, int* counters, cudaStream_t s) {
   using namespace p2;
   auto fn = tensor_map_encoder();
   if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
@@ -378,6 +440,10 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(STAR_ECUDA, "phase2: tensor map encode failed");
   const int QR = (hq / hkv) * lq;
+  const int stage_bytes = STAGES * (d == 128 ? Smem<128>::kStage : Smem<64>::kStage);
+  if (n_splits > 1 && (int64_t)n_splits * QR * 4 + QR * 4 + 16 > stage_bytes)
+    return fail(STAR_ECONFIG, "phase2: %d splits x %d query rows exceed the fix-up buffer", n_splits,
+                QR);
   dim3 grid(n_splits, hkv, batch);
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)d));
   const int64_t part_rows = (int64_t)batch * lq * hq;
@@ -388,7 +454,8 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \
     kern<<<grid, kThreads, bytes, s>>>(tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, pps,  \
-                                       page_size, kv_len, own_tail, chunk, out, lse, part_rows, sl2); \
+                                       page_size, kv_len, own_tail, chunk, out, lse, part_rows, sl2,   \
+                                       final_out, final_lse, counters);                          \
   } while (0)
   if (d == 128) {
     if (QR <= 16) STAR_P2M(128, true); else STAR_P2M(128, false);

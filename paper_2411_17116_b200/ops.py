@@ -167,7 +167,10 @@ def kv_read(k_pages: torch.Tensor, v_pages: torch.Tensor, page_table: torch.Tens
 
 # ---------------------------------------------------------------------------- phase 2
 class Phase2Workspace:
-    """Reusable device workspace for the split partials (sized on demand)."""
+    """Reusable device workspace for the split partials (sized on demand).
+
+    Zero-initialised: the bf16 kernel keeps per-(sequence, head) arrival counters at its
+    tail and leaves them re-armed (zero) after every launch."""
 
     def __init__(self):
         self.buf: torch.Tensor | None = None
@@ -176,7 +179,7 @@ class Phase2Workspace:
         if nbytes <= 0:
             return None
         if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
-            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
         return self.buf.data_ptr()
 
 
