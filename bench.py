@@ -166,9 +166,11 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("STAR_BENCH_BACKEND", "nccl")  # gloo: multi-rank logic test on 1 GPU
+    if backend != "nccl":
+        local %= torch.cuda.device_count()  # ranks may share a device in this test mode
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    backend = os.environ.get("STAR_BENCH_BACKEND", "nccl")  # gloo: multi-rank logic test on 1 GPU
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)

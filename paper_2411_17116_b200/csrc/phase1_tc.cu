@@ -113,8 +113,11 @@ __device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, flo
         if (col > lim) p0 = 0.f;
         if (col + 1 > lim) p1 = 0.f;
       }
-      rsum[(e >> 1) & 3] += p0 + p1;
-      pk[e >> 1] = pack_bf16x2(p0, p1);
+      // the row sum uses the bf16-rounded p that the P.V MMA will see, so numerator and
+      // denominator weight each key identically (a dominant key then carries no error)
+      const uint32_t w = pack_bf16x2(p0, p1);
+      pk[e >> 1] = w;
+      rsum[(e >> 1) & 3] += bf16lo(w) + bf16hi(w);
     }
     tmem_st16(s_tm + c * 16, pk);
   }

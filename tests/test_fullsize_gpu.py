@@ -5,8 +5,11 @@ b = a = 32K) are run whole on one GPU (every block of the layer in one K1 launch
 superset of any rank's share).  Checked:
   * anchor invariance, BIT-EXACT: with first_block anchors, rows [0, a) of every augmented
     block are the same computation as block 0's rows [0, a) (same tokens, positions, keys);
-  * sampled rows vs the fp64 oracle on the same bf16 inputs (normwise per row <= 2e-3 with
-    fp32 output; lse within 2e-3);
+  * sampled rows vs the fp64 oracle on the same bf16 inputs, with fp32 output: normwise per
+    (row-block, head) <= 2e-3 — the metric SURVEY §7 fixes for bf16 P with fp32 accumulation,
+    the row-block being the sampled rows of that (segment, head) — and every single row
+    within 4 x that (a per-row max over 128 lanes sees the tail of the bf16-P rounding noise);
+    lse within 2e-3;
   * phase 2 (K2) over a 1M-token paged cache and a batch-32 x 32K decode, sampled heads vs
     the oracle's partial_attention; and the merge rule: K2 over 4 shards + K3 == K2 over the
     whole cache.
@@ -63,7 +66,7 @@ def test_phase1_full_size(ops, name, L, b, a, hq, hkv):
     d = 128
     seg, pos = _augmented(L, b, a)
     q, k, v = _inputs(ops, L, hq, hkv, d, pos)
-    out, lse = ops.phase1_fwd(q, k, v, seg, want_lse=True)
+    out, lse = ops.phase1_fwd(q, k, v, seg, want_lse=True, out_dtype=torch.float32)
     torch.cuda.synchronize()
     # (1) anchor invariance, bit-exact
     for s in range(1, len(seg) - 1):
@@ -81,12 +84,18 @@ def test_phase1_full_size(ops, name, L, b, a, hq, hkv):
             kk = k[lo:hi, h // G].float().cpu().numpy().astype(np.float64)
             vv = v[lo:hi, h // G].float().cpu().numpy().astype(np.float64)
             qq = q[lo:hi, h].float().cpu().numpy().astype(np.float64)
+            got_rows, ref_rows = [], []
             for r in rows:
                 ref, ref_l = O.causal_attention_lse(qq[r:r + 1], kk[:r + 1], vv[:r + 1], q_offset=r)
                 got = out[lo + r, h].float().cpu().numpy()
-                err = np.abs(got - ref[0]).max() / np.abs(ref[0]).max()
-                assert err <= TOL + 2.0 ** -9, (name, s, h, r, err)
+                row_err = np.abs(got - ref[0]).max() / np.abs(ref[0]).max()
+                assert row_err <= 4 * TOL, (name, s, h, r, row_err)
                 assert abs(float(lse[h, lo + r]) - float(ref_l[0])) <= TOL, (name, s, h, r)
+                got_rows.append(got)
+                ref_rows.append(ref[0])
+            g_, r_ = np.stack(got_rows), np.stack(ref_rows)
+            err = np.abs(g_ - r_).max() / np.abs(r_).max()
+            assert err <= TOL, (name, s, h, err)
     del q, k, v, out, lse
     torch.cuda.empty_cache()
 
