@@ -3,6 +3,7 @@
 // then dispatch to the sm_100a kernels.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -48,6 +49,19 @@ int attention_simt(const void*, const void*, const void*, int, SegTable&, int, i
                    int64_t, int, void*, int, int64_t, float*, int64_t, cudaStream_t);
 int phase1_tc(const void*, const void*, const void*, SegTable&, int, int, int, int64_t, int64_t,
               int64_t, void*, int, int64_t, float*, int64_t, cudaStream_t);
+int phase1_tc64(const void*, const void*, const void*, SegTable&, int, int, int64_t, int64_t,
+                int64_t, void*, int, int64_t, float*, int64_t, cudaStream_t);
+
+// K1 variant: "s128" (128-key tiles, default) or "db64" (64-key tiles, double-buffered S/P
+// in TMEM; correct, measured 7% slower on cfg2 — kept for tuning via STAR_K1_VARIANT=db64).
+static bool use_db64() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("STAR_K1_VARIANT");
+    v = (e != nullptr && e[0] == 'd') ? 1 : 0;  // default: s128 (measured faster)
+  }
+  return v == 1;
+}
 int64_t phase2_workspace_bytes(int, int, int, int, int);
 int phase2_auto_splits(int, int, int64_t, int);
 int phase2_partial(const void*, int, int, int, int, int, int, const void*, const void*, int,
@@ -119,6 +133,9 @@ int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int 
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == STAR_BF16 && (d == 64 || d == 128)) {
     if (total >= (1ll << 31)) return fail(STAR_ENOTSUP, "phase1: more than 2^31 rows per call");
+    if (d == 128 && (hq / hkv) % 2 == 0 && use_db64())
+      return phase1_tc64(q, k, v, segs, hq, hkv, total, q_row_stride, kv_row_stride, out,
+                         out_dtype == STAR_F32, out_row_stride, lse, lse_stride, s);
     return phase1_tc(q, k, v, segs, hq, hkv, d, total, q_row_stride, kv_row_stride, out,
                      out_dtype == STAR_F32, out_row_stride, lse, lse_stride, s);
   }

@@ -27,6 +27,7 @@
 // commit after S_i(j+1) also certifies PV_i(j) (O stable for the rescale).
 
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -95,9 +96,29 @@ __device__ __forceinline__ float row_max(uint32_t s_tm, int lim) {
 
 // Softmax pass 2: p = 2^(s*sl2 - m) per column, row sum, P packed bf16x2 into the TMEM
 // columns of S already consumed (chunk c -> columns [16c, 16c+16)).
-template <bool DIAG>
+// 2^x for a pair on the FMA pipe (offloads the MUFU/XU pipe): x clamped to >= -125,
+// x = n + f with n = round(x) (magic-number rounding), 2^f by a degree-3 minimax
+// polynomial on [-1/2, 1/2] (max rel. error 2.1e-4, below bf16's 2^-9 rounding of P),
+// then n is added to the exponent field with one IMAD.
+__device__ __forceinline__ float2 poly_ex2x2(float2 x) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
+  const float2 r = fadd2(t, make_float2(-kMagic, -kMagic));
+  const float2 f = fadd2(x, make_float2(-r.x, -r.y));
+  float2 p = ffma2(f, make_float2(0.05484800413f, 0.05484800413f),
+                   make_float2(0.24180661142f, 0.24180661142f));
+  p = ffma2(p, f, make_float2(0.69324821234f, 0.69324821234f));
+  p = ffma2(p, f, make_float2(0.99998867512f, 0.99998867512f));
+  return make_float2(__int_as_float(__float_as_int(t.x) * 8388608 + __float_as_int(p.x)),
+                     __int_as_float(__float_as_int(t.y) * 8388608 + __float_as_int(p.y)));
+}
+
+template <bool DIAG, int POLY>
 __device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, float m) {
-  float rsum[4] = {0.f, 0.f, 0.f, 0.f};
+  float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     uint32_t sv[32];
@@ -106,8 +127,16 @@ __device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, flo
     uint32_t pk[16];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
-      float p0 = ex2(fmaf(__uint_as_float(sv[e]), sl2, -m));
-      float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), sl2, -m));
+      const float2 x = ffma2(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), sc2, nm2);
+      float p0, p1;
+      if (c >= 4 - POLY) {
+        const float2 p = poly_ex2x2(x);
+        p0 = p.x;
+        p1 = p.y;
+      } else {
+        p0 = ex2(x.x);
+        p1 = ex2(x.y);
+      }
       if (DIAG) {
         const int col = c * 32 + e;
         if (col > lim) p0 = 0.f;
@@ -117,14 +146,14 @@ __device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, flo
       // denominator weight each key identically (a dominant key then carries no error)
       const uint32_t w = pack_bf16x2(p0, p1);
       pk[e >> 1] = w;
-      rsum[(e >> 1) & 3] += bf16lo(w) + bf16hi(w);
+      rsum[(e >> 1) & 1] = fadd2(rsum[(e >> 1) & 1], make_float2(bf16lo(w), bf16hi(w)));
     }
     tmem_st16(s_tm + c * 16, pk);
   }
-  return (rsum[0] + rsum[1]) + (rsum[2] + rsum[3]);
+  return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
 }
 
-template <int D, int NQ>
+template <int D, int NQ, int POLY>
 __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
     phase1_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                      const __grid_constant__ CUtensorMap tm_k,
@@ -286,8 +315,8 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
         m_use = mx;
       }
       // ---- pass 2: p = 2^(s*sl2 - m), row sum, bf16 P back into TMEM ----
-      const float rs = diag ? exp_pack<true>(s_tm, lim, sl2, m_use)
-                            : exp_pack<false>(s_tm, lim, sl2, m_use);
+      const float rs = diag ? exp_pack<true, POLY>(s_tm, lim, sl2, m_use)
+                            : exp_pack<false, POLY>(s_tm, lim, sl2, m_use);
       if (warp_rescale) {
         // O is stable: s_full(j) was committed after PV(j-1)
 #pragma unroll
@@ -353,6 +382,8 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
 }
 
 // ------------------------------------------------------------------ host
+constexpr int kDefaultPoly = 0;
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (fn == nullptr) {
@@ -412,14 +443,18 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
     prm.segs.tile_start[i + 1] = prm.segs.tile_start[i] + (segs.lq[i] + C::BM - 1) / C::BM;
   const int tiles = prm.segs.tile_start[segs.n];
   if (tiles == 0) return STAR_OK;
-  auto kern = phase1_tc_kernel<D, NQ>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
-    configured = true;
+  // share of each S row whose exp2 runs on the FMA pipe (in 32-column chunks of 4);
+  // STAR_K1_POLY overrides for tuning
+  static int poly = -1;
+  if (poly < 0) {
+    const char* env = getenv("STAR_K1_POLY");
+    poly = env ? atoi(env) : kDefaultPoly;
+    if (poly < 0 || poly > 2) poly = kDefaultPoly;
   }
+  auto kern = poly == 0 ? phase1_tc_kernel<D, NQ, 0>
+                        : (poly == 1 ? phase1_tc_kernel<D, NQ, 1> : phase1_tc_kernel<D, NQ, 2>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
   dim3 grid(hkv * (hq / hkv / NQ), tiles);
   kern<<<grid, C::kThreads, C::kSmem, stream>>>(tq, tk, tv, prm);
   STAR_LAUNCH_CHECK("phase1_tc");

@@ -1,0 +1,94 @@
+"""Host-buffer entry point of the phase-1 encode, pipelined per block.
+
+The reference's phase 1 takes host (numpy) data and returns host data
+(ss/sim.py:126-175).  Called with pinned host tensors, this module overlaps,
+per anchor-augmented block (segment): host->device copy of block i+1, RoPE + K1 +
+own-row KV page write of block i, device->host copy of the output of block i-1 —
+on three CUDA streams ordered by events.  The copies then hide behind the
+tensor-core work instead of adding to it.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import torch
+
+from . import ops
+from .errors import ShapeError
+
+
+@dataclass
+class LayerEncodePlan:
+    """Device buffers and streams for repeated host-buffer encodes of one layer shape."""
+
+    seg: list
+    own: list            # own rows per segment (the tail of each segment)
+    cache_row0: list     # first cache row of each segment's own rows
+    q: torch.Tensor      # device staging, [rows, hq, d]
+    k: torch.Tensor
+    v: torch.Tensor
+    q_rot: torch.Tensor
+    k_rot: torch.Tensor
+    out: torch.Tensor
+    streams: tuple = field(default_factory=tuple)
+
+    @classmethod
+    def create(cls, seg: Sequence[int], own: Sequence[int], hq: int, hkv: int, d: int,
+               device, dtype=torch.bfloat16) -> "LayerEncodePlan":
+        rows = seg[-1]
+        if len(own) != len(seg) - 1:
+            raise ShapeError("one own-row count per segment")
+        c0, acc = [], 0
+        for o in own:
+            c0.append(acc)
+            acc += o
+        mk = lambda h: torch.empty((rows, h, d), dtype=dtype, device=device)  # noqa: E731
+        q, k, v = mk(hq), mk(hkv), mk(hkv)
+        streams = tuple(torch.cuda.Stream(device) for _ in range(3))
+        return cls(list(seg), list(own), c0, q, k, v, torch.empty_like(q), torch.empty_like(k),
+                   torch.empty_like(q), streams)
+
+
+def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch.Tensor,
+                      v_host: torch.Tensor, positions: torch.Tensor, k_pages: torch.Tensor,
+                      v_pages: torch.Tensor, page_table: torch.Tensor, out_host: torch.Tensor,
+                      theta: float = 10000.0) -> None:
+    """Phase-1 encode of one layer from pinned host q/k/v (pre-RoPE) to pinned host out.
+
+    positions: device int64 [rows].  Returns when every copy and kernel is queued; the
+    caller synchronises (or records an event) on the current stream, which is made to wait
+    on the pipeline.
+    """
+    s_in, s_comp, s_out = plan.streams
+    cur = torch.cuda.current_stream(plan.q.device)
+    s_in.wait_stream(cur)
+    s_comp.wait_stream(cur)
+    s_out.wait_stream(cur)
+    n = len(plan.seg) - 1
+    for i in range(n):
+        a, b = plan.seg[i], plan.seg[i + 1]
+        with torch.cuda.stream(s_in):
+            plan.q[a:b].copy_(q_host[a:b], non_blocking=True)
+            plan.k[a:b].copy_(k_host[a:b], non_blocking=True)
+            plan.v[a:b].copy_(v_host[a:b], non_blocking=True)
+        ev_in = torch.cuda.Event()
+        ev_in.record(s_in)
+        with torch.cuda.stream(s_comp):
+            s_comp.wait_event(ev_in)
+            pos = positions[a:b]
+            ops.rope(plan.q[a:b], pos, theta, out=plan.q_rot[a:b])
+            ops.rope(plan.k[a:b], pos, theta, out=plan.k_rot[a:b])
+            ops.phase1_fwd(plan.q_rot[a:b], plan.k_rot[a:b], plan.v[a:b], [0, b - a],
+                           out=plan.out[a:b])
+            lo = b - plan.own[i]
+            ops.kv_write(plan.k_rot[lo:b], plan.v[lo:b], k_pages, v_pages, page_table,
+                         plan.cache_row0[i])
+        ev_c = torch.cuda.Event()
+        ev_c.record(s_comp)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_c)
+            out_host[a:b].copy_(plan.out[a:b], non_blocking=True)
+    cur.wait_stream(s_out)
+    cur.wait_stream(s_comp)
