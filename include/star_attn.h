@@ -76,11 +76,16 @@ int star_rope(const void* x, void* y, int dtype, int64_t rows, int heads, int d,
  * bf16 uses the tcgen05/TMEM/TMA kernel (d in {64,128}); f32 uses the fp32
  * check-mode kernel.  Replaces causal_attention (ss/attention.py:109-122) as
  * driven per (block, layer, head) by _encode_block_channels (ss/sim.py:108-123).
+ * dedup_anchor_rows (anchor dedup): when > 0 the caller guarantees
+ * that rows [0, n) of every segment s >= 1 equal rows [0, n) of segment 0 (q, k
+ * and v — first-block anchor content AND positions); the tensor-core path then
+ * computes those rows once, in segment 0, and writes them to every segment
+ * (bit-identical outputs, ~a(a+1)/2 fewer score pairs per block).  0 = off.
  */
 int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int n_seg,
                     const int64_t* seg_start, int hq, int hkv, int d, int64_t q_row_stride,
                     int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
-                    float* lse, void* stream);
+                    float* lse, int64_t dedup_anchor_rows, void* stream);
 
 /*
  * Dense masked attention, one segment: q rows [lq] at absolute offset

@@ -102,7 +102,7 @@ int star_rope(const void* x, void* y, int dtype, int64_t rows, int heads, int d,
 int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int n_seg,
                     const int64_t* seg_start, int hq, int hkv, int d, int64_t q_row_stride,
                     int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
-                    float* lse, void* stream) {
+                    float* lse, int64_t dedup_anchor_rows, void* stream) {
   int rc = check_heads(hq, hkv, d);
   if (out_dtype != STAR_F32 && out_dtype != STAR_BF16)
     return fail(STAR_ECONFIG, "phase1: unknown out dtype %d", out_dtype);
@@ -131,8 +131,19 @@ int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int 
   const int64_t total = seg_start[n_seg];
   const int64_t lse_stride = total;
   cudaStream_t s = (cudaStream_t)stream;
+  if (dedup_anchor_rows < 0) return fail(STAR_ECONFIG, "phase1: negative dedup_anchor_rows");
+  for (int i = 0; i < n_seg && dedup_anchor_rows > 0; ++i)
+    if (segs.lq[i] < dedup_anchor_rows)
+      return fail(STAR_ESHAPE, "phase1: segment %d shorter than the %lld deduplicated anchor rows",
+                  i, (long long)dedup_anchor_rows);
   if (dtype == STAR_BF16 && (d == 64 || d == 128)) {
     if (total >= (1ll << 31)) return fail(STAR_ENOTSUP, "phase1: more than 2^31 rows per call");
+    // only whole 128-row tiles are deduplicated (the tensor-core kernel's q tile); the
+    // fan-out runs in the s128 kernel
+    segs.dedup_tiles = (int32_t)(dedup_anchor_rows / 128);
+    if (segs.dedup_tiles > 0)
+      return phase1_tc(q, k, v, segs, hq, hkv, d, total, q_row_stride, kv_row_stride, out,
+                       out_dtype == STAR_F32, out_row_stride, lse, lse_stride, s);
     if (d == 128 && (hq / hkv) % 2 == 0 && use_db64())
       return phase1_tc64(q, k, v, segs, hq, hkv, total, q_row_stride, kv_row_stride, out,
                          out_dtype == STAR_F32, out_row_stride, lse, lse_stride, s);

@@ -65,6 +65,10 @@ struct SegTable {
   int32_t lk[kMaxSegments];
   int32_t q_offset[kMaxSegments]; // absolute index of q row 0 relative to k row 0 (causal)
   int32_t tile_start[kMaxSegments + 1];  // cumulative q tiles
+  // anchor dedup: the first dedup_tiles 128-row q tiles of every segment
+  // s >= 1 repeat segment 0's rows exactly (first-block anchors); they are not launched —
+  // segment 0's CTAs write their rows to every segment instead.
+  int32_t dedup_tiles = 0;
 };
 
 }  // namespace star

@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
   const int y = blockIdx.y;
   int s = 0;
   while (s + 1 < prm.segs.n && prm.segs.tile_start[s + 1] <= y) ++s;
-  const int ntq = prm.segs.tile_start[s + 1] - prm.segs.tile_start[s];
+  // q tiles of the segment (launched ones are the heaviest ntq - dedup, highest first)
+  const int ntq = (prm.segs.lq[s] + C::BM - 1) / C::BM;
   const int qt = ntq - 1 - (y - prm.segs.tile_start[s]);
   const int G = prm.hq / prm.hkv;
   const int pairs = G / NQ;
@@ -341,37 +342,44 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
     tc_fence_after();
     const float inv = 1.f / l_run;
     const bool row_ok = qrow < lq && prm.out != nullptr;
-    const int64_t orow_off = (int64_t)(q_row0 + qrow) * prm.out_row_stride + (int64_t)(h0 + i) * D;
+    // segments receiving this row: itself, plus every deduplicated segment for anchor tiles
+    const int n_dst = (s == 0 && qt < prm.segs.dedup_tiles) ? prm.segs.n : 1;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t orr[32];
       tmem_ld32(o_tm + c * 32, orr);
       tmem_wait_ld();
       if (row_ok) {
-        if (prm.out_f32) {
-          float* orow = reinterpret_cast<float*>(prm.out) + orow_off;
+        for (int t = 0; t < n_dst; ++t) {
+          const int64_t orow_off = (int64_t)(prm.segs.q_row0[t == 0 ? s : t] + qrow) *
+                                       prm.out_row_stride + (int64_t)(h0 + i) * D;
+          if (prm.out_f32) {
+            float* orow = reinterpret_cast<float*>(prm.out) + orow_off;
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(orow + c * 32 + e) =
-                make_float4(__uint_as_float(orr[e]) * inv, __uint_as_float(orr[e + 1]) * inv,
-                            __uint_as_float(orr[e + 2]) * inv, __uint_as_float(orr[e + 3]) * inv);
-        } else {
-          __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.out) + orow_off;
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(orow + c * 32 + e) =
+                  make_float4(__uint_as_float(orr[e]) * inv, __uint_as_float(orr[e + 1]) * inv,
+                              __uint_as_float(orr[e + 2]) * inv, __uint_as_float(orr[e + 3]) * inv);
+          } else {
+            __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(prm.out) + orow_off;
 #pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            uint4 w;
-            w.x = pack_bf16x2(__uint_as_float(orr[e + 0]) * inv, __uint_as_float(orr[e + 1]) * inv);
-            w.y = pack_bf16x2(__uint_as_float(orr[e + 2]) * inv, __uint_as_float(orr[e + 3]) * inv);
-            w.z = pack_bf16x2(__uint_as_float(orr[e + 4]) * inv, __uint_as_float(orr[e + 5]) * inv);
-            w.w = pack_bf16x2(__uint_as_float(orr[e + 6]) * inv, __uint_as_float(orr[e + 7]) * inv);
-            *reinterpret_cast<uint4*>(orow + c * 32 + e) = w;
+            for (int e = 0; e < 32; e += 8) {
+              uint4 w;
+              w.x = pack_bf16x2(__uint_as_float(orr[e + 0]) * inv, __uint_as_float(orr[e + 1]) * inv);
+              w.y = pack_bf16x2(__uint_as_float(orr[e + 2]) * inv, __uint_as_float(orr[e + 3]) * inv);
+              w.z = pack_bf16x2(__uint_as_float(orr[e + 4]) * inv, __uint_as_float(orr[e + 5]) * inv);
+              w.w = pack_bf16x2(__uint_as_float(orr[e + 6]) * inv, __uint_as_float(orr[e + 7]) * inv);
+              *reinterpret_cast<uint4*>(orow + c * 32 + e) = w;
+            }
           }
         }
       }
     }
-    if (qrow < lq && prm.lse != nullptr)
-      prm.lse[(int64_t)(h0 + i) * prm.lse_stride + q_row0 + qrow] =
-          (m_run + __log2f(l_run)) * 0.6931471805599453f;
+    if (qrow < lq && prm.lse != nullptr) {
+      const float lv = (m_run + __log2f(l_run)) * 0.6931471805599453f;
+      for (int t = 0; t < n_dst; ++t)
+        prm.lse[(int64_t)(h0 + i) * prm.lse_stride + prm.segs.q_row0[t == 0 ? s : t] + qrow] = lv;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -440,7 +448,8 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
   prm.lse = lse;
   prm.segs.tile_start[0] = 0;
   for (int i = 0; i < segs.n; ++i)
-    prm.segs.tile_start[i + 1] = prm.segs.tile_start[i] + (segs.lq[i] + C::BM - 1) / C::BM;
+    prm.segs.tile_start[i + 1] = prm.segs.tile_start[i] + (segs.lq[i] + C::BM - 1) / C::BM -
+                                 (i > 0 ? segs.dedup_tiles : 0);
   const int tiles = prm.segs.tile_start[segs.n];
   if (tiles == 0) return STAR_OK;
   // share of each S row whose exp2 runs on the FMA pipe (in 32-column chunks of 4);

@@ -81,11 +81,13 @@ def rope(x: torch.Tensor, positions: torch.Tensor, theta: float = 10000.0,
 
 # ---------------------------------------------------------------------------- phase 1
 def phase1_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_start: Sequence[int],
-               out: torch.Tensor | None = None, want_lse: bool = False, out_dtype=None):
+               out: torch.Tensor | None = None, want_lse: bool = False, out_dtype=None,
+               dedup_anchor_rows: int = 0):
     """K1: causal attention of each segment [seg_start[s], seg_start[s+1]) with itself.
 
     q [rows, hq, d], k/v [rows, hkv, d] (same dtype).  Returns (out, lse|None),
-    lse fp32 [hq, rows] natural log.
+    lse fp32 [hq, rows] natural log.  dedup_anchor_rows > 0: rows [0, n) of every later
+    segment equal segment 0's (first-block anchors) and are computed once (exact).
     """
     _cuda(q, k, v, out)
     rq, hq, qs = _rows_view(q, "q")
@@ -108,7 +110,7 @@ def phase1_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_start: Seq
     arr = (ctypes.c_int64 * len(seg))(*seg)
     _lib.call("star_phase1_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), dtype_code(q),
               len(seg) - 1, arr, hq, hkv, d, qs, ks, out.data_ptr(), dtype_code(out), os_,
-              _ptr(lse), _stream(q.device))
+              _ptr(lse), int(dedup_anchor_rows), _stream(q.device))
     return out, lse
 
 

@@ -112,12 +112,23 @@ def _block_rows(blocks):
     return seg, pos
 
 
+def _dedup_rows(plan: BlockPlan, spec: AnchorSpec, blocks) -> int:
+    """Anchor rows shared verbatim with block 0 (first-block content AND positions)."""
+    if spec.content_mode != "first_block" or spec.position_mode != "first_block" or len(blocks) < 2:
+        return 0
+    a = blocks[1].anchor_prefix_len
+    return a if a <= len(blocks[0].token_ids) else 0
+
+
 def run_phase1(tokens, plan: BlockPlan, spec: AnchorSpec, weights: ModelWeights,
-               prng: Prng | None = None, workers: int = 1, page_size: int = 128) -> list[Host]:
+               prng: Prng | None = None, workers: int = 1, page_size: int = 128,
+               anchor_dedup: bool = False) -> list[Host]:
     """Encode all blocks host-locally; no ledger entries (ss/sim.py:126-175).
 
     `workers` is accepted for API compatibility: the device encodes every block
-    of a layer in one launch, and results never depend on it.
+    of a layer in one launch, and results never depend on it.  anchor_dedup (SURVEY §8
+    f3): with first-block anchors every block's anchor rows repeat block 0's computation;
+    compute them once (same results, ~24% fewer phase-1 score pairs at a = b).
     """
     if workers < 1:
         raise ConfigError("workers must be >= 1")
@@ -141,9 +152,10 @@ def run_phase1(tokens, plan: BlockPlan, spec: AnchorSpec, weights: ModelWeights,
     seg, pos = _block_rows(blocks)
     x = embed(weights, [t for bl in blocks for t in bl.token_ids])
     pos_t = torch.tensor(pos, dtype=torch.int64, device=device)
+    dedup = _dedup_rows(plan, spec, blocks) if anchor_dedup else 0
     for li, lw in enumerate(weights.layers):
         q, k, v = project_qkv(x, lw, cfg, pos_t)
-        att, _ = ops.phase1_fwd(q, k, v, seg, out_dtype=torch.float32)
+        att, _ = ops.phase1_fwd(q, k, v, seg, out_dtype=torch.float32, dedup_anchor_rows=dedup)
         for bi, bl in enumerate(blocks):
             lo = seg[bi] + bl.anchor_prefix_len
             host, r = row_of_block[bi]

@@ -44,11 +44,11 @@ def test_status_maps_to_reference_exceptions():
     with pytest.raises(DomainError, match="zero partials"):
         _lib.check(rc)
     seg = (ctypes.c_int64 * 2)(0, 4)
-    rc = lib.star_phase1_fwd(None, None, None, 0, 1, seg, 4, 3, 8, 32, 32, None, 0, 32, None, None)
+    rc = lib.star_phase1_fwd(None, None, None, 0, 1, seg, 4, 3, 8, 32, 32, None, 0, 32, None, 0, None)
     assert rc == _lib.STAR_ESHAPE  # hq not a multiple of hkv
     with pytest.raises(ShapeError):
         _lib.check(rc)
-    rc = lib.star_phase1_fwd(None, None, None, 0, 99, seg, 4, 4, 8, 32, 32, None, 0, 32, None, None)
+    rc = lib.star_phase1_fwd(None, None, None, 0, 99, seg, 4, 4, 8, 32, 32, None, 0, 32, None, 0, None)
     with pytest.raises(ConfigError):
         _lib.check(rc)
     rc = lib.star_rope(None, None, 0, 4, 1, 7, 7, 7, None, 10000.0, None)

@@ -239,3 +239,24 @@ def test_merge_matches_reference(ops, golden_dir):
     outs2 = torch.cat([outs, torch.full_like(outs[:1], 123.0)])
     out2, lse2 = ops.merge(outs2, lses2)
     assert torch.allclose(out2, out) and torch.allclose(lse2, lse)
+
+
+def test_phase1_anchor_dedup_bit_exact(ops):
+    """with first-block anchors the deduplicated launch equals the full one."""
+    hq, hkv, d, a = 8, 2, 128, 384
+    own = [640, 512, 700]
+    seg = [0]
+    for i, o in enumerate(own):
+        seg.append(seg[-1] + o + (a if i else 0))
+    rows = seg[-1]
+    q = torch.randn(rows, hq, d).to(torch.bfloat16)
+    k = torch.randn(rows, hkv, d).to(torch.bfloat16)
+    v = torch.randn(rows, hkv, d).to(torch.bfloat16)
+    for s in range(1, len(own)):  # anchor rows = block 0's first a rows
+        for t in (q, k, v):
+            t[seg[s]:seg[s] + a] = t[:a]
+    q, k, v = q.cuda(), k.cuda(), v.cuda()
+    full, full_l = ops.phase1_fwd(q, k, v, seg, want_lse=True)
+    dd, dd_l = ops.phase1_fwd(q, k, v, seg, want_lse=True, dedup_anchor_rows=a)
+    torch.cuda.synchronize()
+    assert torch.equal(full, dd) and torch.equal(full_l, dd_l)

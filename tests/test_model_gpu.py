@@ -151,3 +151,22 @@ def test_session_bf16_tensor_core_path(S, golden_dir, name):
             assert list(host.channels[0].positions)[:len(g[f"host{hi}_pos_ch0"]) - (20 if hi == 3 else 0)] \
                 == list(g[f"host{hi}_pos_ch0"])[:len(g[f"host{hi}_pos_ch0"]) - (20 if hi == 3 else 0)]
         print(name, "bf16 tokens", toks, "ref", list(g["generated"][:4]), "logit err", err)
+
+
+def test_run_phase1_anchor_dedup_matches(S, golden_dir):
+    g, doc = _case(golden_dir, "tiny_s4")
+    md = doc["model"]
+    w = S.init_model(S.ModelConfig(d_model=md["d_model"], heads=md["heads"], layers=md["layers"],
+                                   seed=md["seed"]))
+    plan = S.partition(doc["sequence_len"], doc["block_size"], doc["hosts"])
+    spec = S.AnchorSpec(anchor_len=doc["anchor"]["anchor_len"])
+    ctx = list(g["context_tokens"])
+    with S.precision("bfloat16"):
+        h_full = S.run_phase1(ctx, plan, spec, w, prng=S.Prng(doc["seed"] ^ O.ANCHOR_SALT))
+        h_dd = S.run_phase1(ctx, plan, spec, w, prng=S.Prng(doc["seed"] ^ O.ANCHOR_SALT),
+                            anchor_dedup=True)
+        for a, b in zip(h_full, h_dd):
+            for li in range(md["layers"]):
+                ka, va = a.pool.dense(li)
+                kb, vb = b.pool.dense(li)
+                assert torch.equal(ka, kb) and torch.equal(va, vb)
