@@ -67,6 +67,21 @@ int star_rope(const void* x, void* y, int dtype, int64_t rows, int heads, int d,
               double theta, void* stream);
 
 /*
+ * Fused phase-1 prologue: RoPE of q [rows, hq, d] and k [rows, hkv, d]
+ * at int64 positions into q_out / k_out, and for every row with cache_rows[r] >= 0
+ * (device int64, nullable = no cache writes) the rotated k and the raw v
+ * [rows, hkv, d] (row stride kv_in_stride, shared with k) written to logical cache
+ * row cache_rows[r] of the paged pool.  Replaces rope_apply on q and k
+ * (ss/toy_model.py:161-162) and the own-row retention (ss/sim.py:117-118) in one pass.
+ */
+int star_rope_qkv(const void* q_in, const void* k_in, const void* v_in, int dtype, int64_t rows,
+                  int hq, int hkv, int d, int64_t q_in_stride, int64_t kv_in_stride, void* q_out,
+                  void* k_out, int64_t q_out_stride, int64_t k_out_stride,
+                  const int64_t* positions, double theta, const int64_t* cache_rows,
+                  void* k_pages, void* v_pages, const int32_t* page_table, int page_size,
+                  void* stream);
+
+/*
  * Phase 1 (K1): causal self-attention over one or more anchor-augmented
  * blocks concatenated along rows.  Segment s covers rows
  * [seg_start[s], seg_start[s+1]) of q/k/v/out (seg_start: HOST array of

@@ -25,6 +25,9 @@ SIGNATURES = {
     "star_prng_fill": (c_int, [c_void_p, c_int, c_int64, c_uint64, c_uint64, c_double, c_void_p]),
     "star_rope": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int, c_int, c_int64, c_int64,
                           c_void_p, c_double, c_void_p]),
+    "star_rope_qkv": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int, c_int, c_int,
+                              c_int64, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_void_p,
+                              c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "star_phase1_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, POINTER(c_int64),
                                 c_int, c_int, c_int, c_int64, c_int64, c_void_p, c_int, c_int64,
                                 c_void_p, c_int64, c_void_p]),

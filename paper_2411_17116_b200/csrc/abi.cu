@@ -43,6 +43,9 @@ int rope(const void*, void*, int, int64_t, int, int, int64_t, int64_t, const int
          cudaStream_t);
 int kv_write(const void*, const void*, int, int64_t, int, int, int64_t, void*, void*,
              const int32_t*, int, int64_t, cudaStream_t);
+int rope_qkv(const void*, const void*, const void*, int, int64_t, int, int, int, int64_t, int64_t,
+             void*, void*, int64_t, int64_t, const int64_t*, double, const int64_t*, void*, void*,
+             const int32_t*, int, cudaStream_t);
 int kv_read(const void*, const void*, int, const int32_t*, int, int64_t, int64_t, int, int, void*,
             void*, cudaStream_t);
 int attention_simt(const void*, const void*, const void*, int, SegTable&, int, int, int, int64_t,
@@ -97,6 +100,17 @@ int star_rope(const void* x, void* y, int dtype, int64_t rows, int heads, int d,
               void* stream) {
   return rope(x, y, dtype, rows, heads, d, x_row_stride, y_row_stride, positions, theta,
               (cudaStream_t)stream);
+}
+
+int star_rope_qkv(const void* q_in, const void* k_in, const void* v_in, int dtype, int64_t rows,
+                  int hq, int hkv, int d, int64_t q_in_stride, int64_t kv_in_stride, void* q_out,
+                  void* k_out, int64_t q_out_stride, int64_t k_out_stride,
+                  const int64_t* positions, double theta, const int64_t* cache_rows,
+                  void* k_pages, void* v_pages, const int32_t* page_table, int page_size,
+                  void* stream) {
+  return rope_qkv(q_in, k_in, v_in, dtype, rows, hq, hkv, d, q_in_stride, kv_in_stride, q_out,
+                  k_out, q_out_stride, k_out_stride, positions, theta, cache_rows, k_pages,
+                  v_pages, page_table, page_size, (cudaStream_t)stream);
 }
 
 int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int n_seg,

@@ -98,6 +98,88 @@ int rope(const void* x, void* y, int dtype, int64_t rows, int heads, int d, int6
   return STAR_OK;
 }
 
+// ------------------------------------------------------------------ fused prologue
+// one pass over the projection outputs of a layer's augmented blocks —
+// RoPE of every q and k head at the row's position (angle formed once per (row, pair)),
+// rotated q/k written for K1, and for own (cached) rows the rotated k and raw v written
+// straight into the paged cache.  Replaces rope(q) + rope(k) + kv_write.
+template <typename T>
+__global__ void rope_qkv_kernel(const T* __restrict__ qi, const T* __restrict__ ki,
+                                const T* __restrict__ vi, T* __restrict__ qo, T* __restrict__ ko,
+                                int64_t rows, int hq, int hkv, int d, int64_t qis, int64_t kis,
+                                int64_t qos, int64_t kos, const int64_t* __restrict__ pos,
+                                double theta, const int64_t* __restrict__ cache_rows,
+                                T* __restrict__ kp, T* __restrict__ vp,
+                                const int32_t* __restrict__ table, int page_size) {
+  const int half = d >> 1;
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * half) return;
+  int64_t r = idx / half;
+  int i = (int)(idx - r * half);
+  double sn, cs;
+  sincos((double)pos[r] * pow(theta, -2.0 * (double)i / (double)d), &sn, &cs);
+  const T* q = qi + r * qis + 2 * i;
+  T* qw = qo + r * qos + 2 * i;
+  for (int h = 0; h < hq; ++h) {
+    const double x0 = Elem<T>::to_f(q[h * d]), x1 = Elem<T>::to_f(q[h * d + 1]);
+    qw[h * d] = Elem<T>::from_f(__double2float_rn(x0 * cs - x1 * sn));
+    qw[h * d + 1] = Elem<T>::from_f(__double2float_rn(x0 * sn + x1 * cs));
+  }
+  const int64_t cr = cache_rows != nullptr ? cache_rows[r] : -1;
+  T* kpr = nullptr;
+  T* vpr = nullptr;
+  if (cr >= 0) {
+    const int64_t page = table[cr / page_size];
+    const int64_t slot = cr % page_size;
+    kpr = kp + (page * hkv * page_size + slot) * d + 2 * i;
+    vpr = vp + (page * hkv * page_size + slot) * d + 2 * i;
+  }
+  const T* k = ki + r * kis + 2 * i;
+  const T* v = vi + r * kis + 2 * i;
+  T* kw = ko + r * kos + 2 * i;
+  for (int h = 0; h < hkv; ++h) {
+    const double x0 = Elem<T>::to_f(k[h * d]), x1 = Elem<T>::to_f(k[h * d + 1]);
+    const T y0 = Elem<T>::from_f(__double2float_rn(x0 * cs - x1 * sn));
+    const T y1 = Elem<T>::from_f(__double2float_rn(x0 * sn + x1 * cs));
+    kw[h * d] = y0;
+    kw[h * d + 1] = y1;
+    if (kpr != nullptr) {
+      const int64_t po = (int64_t)h * page_size * d;
+      kpr[po] = y0;
+      kpr[po + 1] = y1;
+      vpr[po] = v[h * d];
+      vpr[po + 1] = v[h * d + 1];
+    }
+  }
+}
+
+int rope_qkv(const void* qi, const void* ki, const void* vi, int dtype, int64_t rows, int hq,
+             int hkv, int d, int64_t qis, int64_t kis, void* qo, void* ko, int64_t qos,
+             int64_t kos, const int64_t* pos, double theta, const int64_t* cache_rows, void* kp,
+             void* vp, const int32_t* table, int page_size, cudaStream_t s) {
+  if (d < 2 || (d & 1)) return fail(STAR_ECONFIG, "rope head_dim must be even and >= 2, got %d", d);
+  if (!(theta > 0)) return fail(STAR_ECONFIG, "rope theta must be positive, got %g", theta);
+  if (rows < 0 || hq < 1 || hkv < 1) return fail(STAR_ESHAPE, "rope_qkv: bad shape");
+  if (qis < (int64_t)hq * d || qos < (int64_t)hq * d || kis < (int64_t)hkv * d ||
+      kos < (int64_t)hkv * d)
+    return fail(STAR_ESHAPE, "rope_qkv: row stride smaller than heads*d");
+  if (cache_rows != nullptr && (kp == nullptr || vp == nullptr || table == nullptr || page_size < 1))
+    return fail(STAR_ESHAPE, "rope_qkv: cache rows given without a paged cache");
+  if (rows == 0) return STAR_OK;
+  const int64_t n = rows * (d / 2);
+  const int grid = (int)((n + 255) / 256);
+#define STAR_RQKV(T)                                                                              rope_qkv_kernel<T><<<grid, 256, 0, s>>>((const T*)qi, (const T*)ki, (const T*)vi, (T*)qo,                                               (T*)ko, rows, hq, hkv, d, qis, kis, qos, kos, pos,                                              theta, cache_rows, (T*)kp, (T*)vp, table, page_size)
+  if (dtype == STAR_F32)
+    STAR_RQKV(float);
+  else if (dtype == STAR_BF16)
+    STAR_RQKV(__nv_bfloat16);
+  else
+    return fail(STAR_ECONFIG, "rope_qkv: unknown dtype %d", dtype);
+#undef STAR_RQKV
+  STAR_LAUNCH_CHECK("rope_qkv");
+  return STAR_OK;
+}
+
 // ------------------------------------------------------------------ paged KV
 // Vector width W bytes; each thread moves one W-byte chunk of one (row, head).
 template <typename V>

@@ -79,6 +79,39 @@ def rope(x: torch.Tensor, positions: torch.Tensor, theta: float = 10000.0,
     return out
 
 
+def rope_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, positions: torch.Tensor,
+             theta: float = 10000.0, q_out: torch.Tensor | None = None,
+             k_out: torch.Tensor | None = None, cache_rows: torch.Tensor | None = None,
+             k_pages: torch.Tensor | None = None, v_pages: torch.Tensor | None = None,
+             page_table: torch.Tensor | None = None):
+    """Fused prologue: rotated (q, k) for K1 + own-row (rotated k, v) into pages."""
+    _cuda(q, k, v, positions, cache_rows, k_pages, v_pages, page_table)
+    rows, hq, qs = _rows_view(q, "q")
+    rk, hkv, ks = _rows_view(k, "k")
+    if rk != rows or tuple(v.shape) != tuple(k.shape) or v.stride() != k.stride():
+        raise ShapeError("q/k/v rows or k/v layouts disagree")
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ConfigError("q, k, v must share a dtype")
+    if positions.dtype != torch.int64 or positions.numel() != rows:
+        raise ShapeError(f"{positions.numel()} positions for {rows} rows (int64 required)")
+    q_out = torch.empty_like(q) if q_out is None else q_out
+    k_out = torch.empty_like(k) if k_out is None else k_out
+    _, _, qos = _rows_view(q_out, "q_out")
+    _, _, kos = _rows_view(k_out, "k_out")
+    page_size = 0
+    if cache_rows is not None:
+        if cache_rows.dtype != torch.int64 or cache_rows.numel() != rows:
+            raise ShapeError("cache_rows must be int64 [rows]")
+        if k_pages is None or k_pages.dtype != k.dtype or k_pages.shape[1] != hkv:
+            raise ShapeError("paged pool does not match k")
+        page_size = k_pages.shape[2]
+    _lib.call("star_rope_qkv", q.data_ptr(), k.data_ptr(), v.data_ptr(), dtype_code(q), rows, hq,
+              hkv, q.shape[2], qs, ks, q_out.data_ptr(), k_out.data_ptr(), qos, kos,
+              positions.contiguous().data_ptr(), float(theta), _ptr(cache_rows), _ptr(k_pages),
+              _ptr(v_pages), _ptr(page_table), page_size, _stream(q.device))
+    return q_out, k_out
+
+
 # ---------------------------------------------------------------------------- phase 1
 def phase1_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_start: Sequence[int],
                out: torch.Tensor | None = None, want_lse: bool = False, out_dtype=None,

@@ -2,8 +2,8 @@
 
 The reference's phase 1 takes host (numpy) data and returns host data
 (ss/sim.py:126-175).  Called with pinned host tensors, this module overlaps,
-per anchor-augmented block (segment): host->device copy of block i+1, RoPE + K1 +
-own-row KV page write of block i, device->host copy of the output of block i-1 —
+per anchor-augmented block (segment): host->device copy of block i+1, the fused
+prologue (RoPE + own-row KV page write) and K1 of block i, device->host copy of the output of block i-1 —
 on three CUDA streams ordered by events.  The copies then hide behind the
 tensor-core work instead of adding to it.
 """
@@ -32,6 +32,7 @@ class LayerEncodePlan:
     q_rot: torch.Tensor
     k_rot: torch.Tensor
     out: torch.Tensor
+    cache_rows: torch.Tensor  # logical cache row per augmented row, -1 for anchor rows
     streams: tuple = field(default_factory=tuple)
 
     @classmethod
@@ -46,9 +47,12 @@ class LayerEncodePlan:
             acc += o
         mk = lambda h: torch.empty((rows, h, d), dtype=dtype, device=device)  # noqa: E731
         q, k, v = mk(hq), mk(hkv), mk(hkv)
+        cr = torch.full((rows,), -1, dtype=torch.int64)
+        for i, o in enumerate(own):
+            cr[seg[i + 1] - o:seg[i + 1]] = torch.arange(c0[i], c0[i] + o)
         streams = tuple(torch.cuda.Stream(device) for _ in range(3))
         return cls(list(seg), list(own), c0, q, k, v, torch.empty_like(q), torch.empty_like(k),
-                   torch.empty_like(q), streams)
+                   torch.empty_like(q), cr.to(device), streams)
 
 
 def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch.Tensor,
@@ -77,14 +81,12 @@ def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch
         ev_in.record(s_in)
         with torch.cuda.stream(s_comp):
             s_comp.wait_event(ev_in)
-            pos = positions[a:b]
-            ops.rope(plan.q[a:b], pos, theta, out=plan.q_rot[a:b])
-            ops.rope(plan.k[a:b], pos, theta, out=plan.k_rot[a:b])
+            ops.rope_qkv(plan.q[a:b], plan.k[a:b], plan.v[a:b], positions[a:b], theta,
+                         q_out=plan.q_rot[a:b], k_out=plan.k_rot[a:b],
+                         cache_rows=plan.cache_rows[a:b], k_pages=k_pages, v_pages=v_pages,
+                         page_table=page_table)
             ops.phase1_fwd(plan.q_rot[a:b], plan.k_rot[a:b], plan.v[a:b], [0, b - a],
                            out=plan.out[a:b])
-            lo = b - plan.own[i]
-            ops.kv_write(plan.k_rot[lo:b], plan.v[lo:b], k_pages, v_pages, page_table,
-                         plan.cache_row0[i])
         ev_c = torch.cuda.Event()
         ev_c.record(s_comp)
         with torch.cuda.stream(s_out):

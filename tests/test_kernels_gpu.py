@@ -260,3 +260,30 @@ def test_phase1_anchor_dedup_bit_exact(ops):
     dd, dd_l = ops.phase1_fwd(q, k, v, seg, want_lse=True, dedup_anchor_rows=a)
     torch.cuda.synchronize()
     assert torch.equal(full, dd) and torch.equal(full_l, dd_l)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_fused_prologue_equals_rope_plus_kv_write(ops, dtype):
+    """rope_qkv == rope(q), rope(k) and kv_write of the cached rows, bit-exact."""
+    rows, hq, hkv, d, page = 300, 8, 2, 128, 64
+    rng = np.random.default_rng(11)
+    q = torch.randn(rows, hq, d).to(dtype).cuda()
+    k = torch.randn(rows, hkv, d).to(dtype).cuda()
+    v = torch.randn(rows, hkv, d).to(dtype).cuda()
+    pos = torch.from_numpy(rng.integers(0, 1 << 20, rows)).cuda()
+    cache_rows = torch.full((rows,), -1, dtype=torch.int64)
+    cache_rows[100:] = torch.arange(200)  # the last 200 rows are "own" rows
+    cache_rows = cache_rows.cuda()
+    n_pages = 5
+    table = torch.tensor([3, 1, 4, 0], dtype=torch.int32).cuda()
+    kp = torch.zeros((n_pages, hkv, page, d), dtype=dtype, device="cuda")
+    vp = torch.zeros_like(kp)
+    qo, ko = ops.rope_qkv(q, k, v, pos, cache_rows=cache_rows, k_pages=kp, v_pages=vp,
+                          page_table=table)
+    q_ref = ops.rope(q, pos)
+    k_ref = ops.rope(k, pos)
+    kp2, vp2 = torch.zeros_like(kp), torch.zeros_like(vp)
+    ops.kv_write(k_ref[100:], v[100:], kp2, vp2, table, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(qo, q_ref) and torch.equal(ko, k_ref)
+    assert torch.equal(kp, kp2) and torch.equal(vp, vp2)
