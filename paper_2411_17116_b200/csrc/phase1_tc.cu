@@ -176,17 +176,22 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- work item: (segment, q tile) from blockIdx.y (heavy tiles first), head group x ----
-  const int y = blockIdx.y;
-  int s = 0;
-  while (s + 1 < prm.segs.n && prm.segs.tile_start[s + 1] <= y) ++s;
-  // q tiles of the segment (launched ones are the heaviest ntq - dedup, highest first)
-  const int ntq = (prm.segs.lq[s] + C::BM - 1) / C::BM;
-  const int qt = ntq - 1 - (y - prm.segs.tile_start[s]);
+  // ---- work item from a 1-D raster: segment-major, then kv head, then q tile (heaviest
+  // first), then the head pair — CTAs resident together share one kv head's K/V, which
+  // stays L2-resident (a block's K/V over all kv heads exceeds the 126 MB L2) ----
   const int G = prm.hq / prm.hkv;
   const int pairs = G / NQ;
-  const int kvh = blockIdx.x / pairs;
-  const int h0 = kvh * G + (blockIdx.x % pairs) * NQ;
+  const int per_tile = prm.hkv * pairs;  // CTAs per launched q tile
+  const int bx = blockIdx.x;
+  int s = 0;
+  while (s + 1 < prm.segs.n && prm.segs.tile_start[s + 1] * per_tile <= bx) ++s;
+  const int ntq = (prm.segs.lq[s] + C::BM - 1) / C::BM;
+  const int launched = prm.segs.tile_start[s + 1] - prm.segs.tile_start[s];
+  const int loc = bx - prm.segs.tile_start[s] * per_tile;  // [0, hkv * launched * pairs)
+  const int kvh = loc / (launched * pairs);
+  const int rem = loc - kvh * launched * pairs;
+  const int qt = ntq - 1 - rem / pairs;
+  const int h0 = kvh * G + (rem % pairs) * NQ;
   const int lq = prm.segs.lq[s];
   const int q_row0 = (int)prm.segs.q_row0[s];
   const int k_row0 = (int)prm.segs.k_row0[s];
@@ -464,7 +469,7 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
                         : (poly == 1 ? phase1_tc_kernel<D, NQ, 1> : phase1_tc_kernel<D, NQ, 2>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
-  dim3 grid(hkv * (hq / hkv / NQ), tiles);
+  dim3 grid(tiles * hkv * (hq / hkv / NQ));
   kern<<<grid, C::kThreads, C::kSmem, stream>>>(tq, tk, tv, prm);
   STAR_LAUNCH_CHECK("phase1_tc");
   return STAR_OK;
