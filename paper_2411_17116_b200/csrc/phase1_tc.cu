@@ -68,34 +68,31 @@ struct P1Params {
 };
 
 // Softmax pass 1 over one 128-column S row in TMEM: max of the (masked) raw scores.
+// Loads are software-pipelined: chunk c+1 is in flight while chunk c is reduced.
 template <bool DIAG>
 __device__ __forceinline__ float row_max(uint32_t s_tm, int lim) {
-  uint32_t a[32], b[32];
+  uint32_t buf[2][32];
   float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  tmem_ld32(s_tm, buf[0]);
+  tmem_wait_ld_tied(buf[0]);
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    tmem_ld32(s_tm + half * 64, a);
-    tmem_ld32(s_tm + half * 64 + 32, b);
-    tmem_wait_ld();
+  for (int c = 0; c < 4; ++c) {
+    if (c < 3) tmem_ld32(s_tm + (c + 1) * 32, buf[(c + 1) & 1]);
+    uint32_t* a = buf[c & 1];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
-      float va0 = __uint_as_float(a[e]), va1 = __uint_as_float(a[e + 1]);
-      float vb0 = __uint_as_float(b[e]), vb1 = __uint_as_float(b[e + 1]);
+      float v0 = __uint_as_float(a[e]), v1 = __uint_as_float(a[e + 1]);
       if (DIAG) {
-        const int c = half * 64 + e;
-        if (c > lim) va0 = -INFINITY;
-        if (c + 1 > lim) va1 = -INFINITY;
-        if (c + 32 > lim) vb0 = -INFINITY;
-        if (c + 33 > lim) vb1 = -INFINITY;
+        if (c * 32 + e > lim) v0 = -INFINITY;
+        if (c * 32 + e + 1 > lim) v1 = -INFINITY;
       }
-      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(fmaxf(va0, va1), fmaxf(vb0, vb1)));
+      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(v0, v1));
     }
+    if (c < 3) tmem_wait_ld_tied(buf[(c + 1) & 1]);
   }
   return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
 }
 
-// Softmax pass 2: p = 2^(s*sl2 - m) per column, row sum, P packed bf16x2 into the TMEM
-// columns of S already consumed (chunk c -> columns [16c, 16c+16)).
 // 2^x for a pair on the FMA pipe (offloads the MUFU/XU pipe): x clamped to >= -125,
 // x = n + f with n = round(x) (magic-number rounding), 2^f by a degree-3 minimax
 // polynomial on [-1/2, 1/2] (max rel. error 2.1e-4, below bf16's 2^-9 rounding of P),
@@ -119,11 +116,15 @@ template <bool DIAG, int POLY>
 __device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, float m) {
   float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+  uint32_t buf[2][32];
+  tmem_ld32(s_tm, buf[0]);
+  tmem_wait_ld_tied(buf[0]);
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    uint32_t sv[32];
-    tmem_ld32(s_tm + c * 32, sv);
-    tmem_wait_ld();
+    // chunk c+1 loads while chunk c is exponentiated; P of chunk c goes to columns
+    // [16c, 16c+16), all below the columns still being read
+    if (c < 3) tmem_ld32(s_tm + (c + 1) * 32, buf[(c + 1) & 1]);
+    const uint32_t* sv = buf[c & 1];
     uint32_t pk[16];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
@@ -149,6 +150,7 @@ __device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, flo
       rsum[(e >> 1) & 1] = fadd2(rsum[(e >> 1) & 1], make_float2(bf16lo(w), bf16hi(w)));
     }
     tmem_st16(s_tm + c * 16, pk);
+    if (c < 3) tmem_wait_ld_tied(buf[(c + 1) & 1]);
   }
   return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
 }
