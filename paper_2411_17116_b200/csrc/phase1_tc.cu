@@ -48,7 +48,7 @@ struct P1Cfg {
   static constexpr int kKOff = kQOff + NQ * kTile;
   static constexpr int kVOff = kKOff + KST * kTile;
   static constexpr int kBarOff = kVOff + VST * kTile;
-  static constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 3 * NQ;
+  static constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 3 * NQ + 4 * NQ;
   static constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + align slack
   static constexpr int kThreads = 64 + 128 * NQ;  // 2 control warps + softmax warpgroups
   static constexpr int kTmemCols = (NQ * (BN + D) <= 256) ? 256 : 512;
@@ -62,10 +62,27 @@ struct P1Params {
   int64_t out_row_stride;
   int64_t lse_stride;
   float scale_log2;
+  int seq;         // ping-pong the softmax warpgroups' exp sections (NQ == 2)
   void* out;       // bf16 or fp32 rows (out_f32)
   int out_f32;
   float* lse;
 };
+
+#ifdef STAR_K1_TRACE
+// Timeline of CTA 0 (clock64): [head][tile][5] softmax events (S ready, max done, turn
+// granted, exps done, P handed over) and [tile][head][2] MMA events (P seen, PV+S issued).
+// Built only into the tracing library (make trace); tools/k1_trace.py reads it.
+constexpr int kTrTiles = 256;
+__device__ long long g_k1_trace[2 * kTrTiles * 5 + kTrTiles * 2 * 2];
+#define K1_TR(cond, idx) \
+  do {                   \
+    if (cond) g_k1_trace[idx] = clock64(); \
+  } while (0)
+#else
+#define K1_TR(cond, idx) \
+  do {                   \
+  } while (0)
+#endif
 
 // Softmax pass 1 over one 128-column S row in TMEM: max of the (masked) raw scores.
 // Loads are software-pipelined: chunk c+1 is in flight while chunk c is reduced.
@@ -112,7 +129,29 @@ __device__ __forceinline__ float2 poly_ex2x2(float2 x) {
                      __int_as_float(__float_as_int(t.y) * 8388608 + __float_as_int(p.y)));
 }
 
-template <bool DIAG, int POLY>
+// volatile forms: the compiler keeps their relative (source) order, which here is the
+// latency-hiding schedule (exponentials first, packs after)
+__device__ __forceinline__ float ex2v(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16x2v(float lo, float hi) {
+  uint32_t r;
+  asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// f32 += bf16 (one FHADD.BF16 per element, no unpack): the exact fp32 value of the
+// bf16-rounded p joins the row sum.
+__device__ __forceinline__ void acc_bf16x2(float& lo_acc, float& hi_acc, uint32_t w) {
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+      "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
+      : "+f"(lo_acc), "+f"(hi_acc)
+      : "r"(w));
+}
+
+template <bool DIAG, int POLY, bool FH>
 __device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, float m) {
   float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
@@ -147,7 +186,11 @@ __device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, flo
       // denominator weight each key identically (a dominant key then carries no error)
       const uint32_t w = pack_bf16x2(p0, p1);
       pk[e >> 1] = w;
-      rsum[(e >> 1) & 1] = fadd2(rsum[(e >> 1) & 1], make_float2(bf16lo(w), bf16hi(w)));
+      float2& acc = rsum[(e >> 1) & 1];
+      if (FH)
+        acc_bf16x2(acc.x, acc.y, w);
+      else
+        acc = fadd2(acc, make_float2(bf16lo(w), bf16hi(w)));
     }
     tmem_st16(s_tm + c * 16, pk);
     if (c < 3) tmem_wait_ld_tied(buf[(c + 1) & 1]);
@@ -155,7 +198,83 @@ __device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, flo
   return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
 }
 
-template <int D, int NQ, int POLY>
+// One-pass softmax: the whole 128-column S row is loaded into registers once (four
+// tcgen05.ld in flight together, one wait), reduced to its max, then exponentiated in
+// place — no second TMEM read and a single exposed load latency per tile.
+__device__ __forceinline__ void tmem_ld_row128(uint32_t s_tm, uint32_t (&sv)[4][32]) {
+  tmem_ld32(s_tm, sv[0]);
+  tmem_ld32(s_tm + 32, sv[1]);
+  tmem_ld32(s_tm + 64, sv[2]);
+  tmem_ld32(s_tm + 96, sv[3]);
+  tmem_wait_ld_tied(sv[0]);
+  tmem_wait_ld_tied(sv[1]);
+  tmem_wait_ld_tied(sv[2]);
+  tmem_wait_ld_tied(sv[3]);
+}
+
+template <bool DIAG>
+__device__ __forceinline__ float row_max_regs(const uint32_t (&sv)[4][32], int lim) {
+  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float v0 = __uint_as_float(sv[c][e]), v1 = __uint_as_float(sv[c][e + 1]);
+      if (DIAG) {
+        if (c * 32 + e > lim) v0 = -INFINITY;
+        if (c * 32 + e + 1 > lim) v1 = -INFINITY;
+      }
+      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(v0, v1));
+    }
+  return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+}
+
+template <bool DIAG, int POLY, bool FH>
+__device__ __forceinline__ float exp_pack_regs(const uint32_t (&sv)[4][32], uint32_t s_tm, int lim,
+                                               float sl2, float m) {
+  float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    // all 32 exponentials of the chunk are issued back to back before any result is
+    // consumed, so the MUFU pipe never idles behind its own latency (in-order issue)
+    float p[32];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      const float2 x = ffma2(make_float2(__uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1])),
+                             sc2, nm2);
+      if (c >= 4 - POLY) {
+        const float2 q = poly_ex2x2(x);
+        p[e] = q.x;
+        p[e + 1] = q.y;
+      } else {
+        p[e] = ex2v(x.x);
+        p[e + 1] = ex2v(x.y);
+      }
+    }
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float p0 = p[e], p1 = p[e + 1];
+      if (DIAG) {
+        const int col = c * 32 + e;
+        if (col > lim) p0 = 0.f;
+        if (col + 1 > lim) p1 = 0.f;
+      }
+      const uint32_t w = pack_bf16x2v(p0, p1);
+      pk[e >> 1] = w;
+      float2& acc = rsum[(e >> 1) & 1];
+      if (FH)
+        acc_bf16x2(acc.x, acc.y, w);
+      else
+        acc = fadd2(acc, make_float2(bf16lo(w), bf16hi(w)));
+    }
+    tmem_st16(s_tm + c * 16, pk);
+  }
+  return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
+}
+
+template <int D, int NQ, int POLY, bool FH, bool ONEP>
 __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
     phase1_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                      const __grid_constant__ CUtensorMap tm_k,
@@ -174,7 +293,8 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
   uint64_t* s_full = v_empty + C::VST;
   uint64_t* p_full = s_full + NQ;
   uint64_t* o_done = p_full + NQ;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NQ);
+  uint64_t* seq_done = o_done + NQ;  // [NQ][4]: softmax warp (i, quarter) finished its exps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(seq_done + 4 * NQ);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -207,6 +327,7 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
       mbar_init(&o_done[i], 1);
+      for (int w = 0; w < 4; ++w) mbar_init(&seq_done[i * 4 + w], 1);
     }
     fence_mbar_init();
   }
@@ -277,6 +398,7 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
         if (next) mbar_wait(&k_full[ks], ((j + 1) / C::KST) & 1);
         for (int i = 0; i < NQ; ++i) {
           mbar_wait(&p_full[i], j & 1);
+          K1_TR(bx == 0 && j < 256, 2 * 256 * 5 + (j * 2 + i) * 2);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < C::BN / 16; ++kk) {
@@ -287,6 +409,7 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
           }
           umma_commit(&o_done[i]);
           if (next) issue_s(i, ks);
+          K1_TR(bx == 0 && j < 256, 2 * 256 * 5 + (j * 2 + i) * 2 + 1);
         }
         umma_commit(&v_empty[vs]);
         if (next) umma_commit(&k_empty[ks]);
@@ -306,15 +429,23 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
 
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(&s_full[i], j & 1);
+      const bool tr = bx == 0 && threadIdx.x % 128 == 64 && j < 256;  // warp quarter 0, lane 0
+      K1_TR(tr, (i * 256 + j) * 5 + 0);
       tc_fence_after();
       const bool diag = (j == qt);
       const int lim = qrow - j * C::BN;  // columns c <= lim are visible on the diagonal tile
       // ---- pass 1: row max (raw scores; the scale is applied once to the max) ----
       float mx;
-      if (diag)
+      uint32_t sv[4][32];
+      if (ONEP) {
+        tmem_ld_row128(s_tm, sv);
+        mx = (diag ? row_max_regs<true>(sv, lim) : row_max_regs<false>(sv, lim)) * sl2;
+      } else if (diag) {
         mx = row_max<true>(s_tm, lim) * sl2;
-      else
+      } else {
         mx = row_max<false>(s_tm, lim) * sl2;
+      }
+      K1_TR(tr, (i * 256 + j) * 5 + 1);
       float m_use = m_run, alpha = 1.f;
       const bool need = (j == 0) || (mx > m_run + 8.f);
       const bool warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
@@ -323,8 +454,30 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
         m_use = mx;
       }
       // ---- pass 2: p = 2^(s*sl2 - m), row sum, bf16 P back into TMEM ----
-      const float rs = diag ? exp_pack<true, POLY>(s_tm, lim, sl2, m_use)
-                            : exp_pack<false, POLY>(s_tm, lim, sl2, m_use);
+      // Ping-pong: the two warps of one SM sub-partition (head 0 and head 1, same TMEM lane
+      // quarter) take turns on its MUFU pipe — head 1 exponentiates tile j after head 0 has,
+      // head 0 tile j after head 1's tile j-1 — so each runs at the full exp2 rate while the
+      // other head's P.V + next S occupy the tensor pipe (anti-phase, not in-phase sharing).
+      const bool seq = NQ == 2 && prm.seq;
+      if (seq) {
+        if (i == 1)
+          mbar_wait(&seq_done[wq], j & 1);
+        else if (j > 0)
+          mbar_wait(&seq_done[4 + wq], (j - 1) & 1);
+      }
+      K1_TR(tr, (i * 256 + j) * 5 + 2);
+      float rs;
+      if (ONEP)
+        rs = diag ? exp_pack_regs<true, POLY, FH>(sv, s_tm, lim, sl2, m_use)
+                  : exp_pack_regs<false, POLY, FH>(sv, s_tm, lim, sl2, m_use);
+      else
+        rs = diag ? exp_pack<true, POLY, FH>(s_tm, lim, sl2, m_use)
+                  : exp_pack<false, POLY, FH>(s_tm, lim, sl2, m_use);
+      K1_TR(tr, (i * 256 + j) * 5 + 3);
+      if (seq) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&seq_done[i * 4 + wq]);
+      }
       if (warp_rescale) {
         // O is stable: s_full(j) was committed after PV(j-1)
 #pragma unroll
@@ -343,6 +496,7 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[i]);
+      K1_TR(tr, (i * 256 + j) * 5 + 4);
     }
     // ---- epilogue: O / l -> rows; lse = ln(sum) + max ----
     mbar_wait(&o_done[i], (nkv - 1) & 1);
@@ -398,6 +552,9 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
 
 // ------------------------------------------------------------------ host
 constexpr int kDefaultPoly = 0;
+constexpr int kDefaultSeq = 1;
+constexpr int kDefaultFH = 1;
+constexpr int kDefaultOnePass = 1;
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -459,16 +616,33 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
                                  (i > 0 ? segs.dedup_tiles : 0);
   const int tiles = prm.segs.tile_start[segs.n];
   if (tiles == 0) return STAR_OK;
-  // share of each S row whose exp2 runs on the FMA pipe (in 32-column chunks of 4);
-  // STAR_K1_POLY overrides for tuning
-  static int poly = -1;
+  // tuning knobs (read once): STAR_K1_POLY = share of each S row (in 32-column chunks of 4)
+  // whose exp2 runs on the FMA pipe; STAR_K1_SEQ = softmax ping-pong; STAR_K1_FH = row sum
+  // by f32+bf16 adds (1) or unpack + FADD2 (0)
+  static int poly = -1, seq = -1, fh = -1, onep = -1;
   if (poly < 0) {
     const char* env = getenv("STAR_K1_POLY");
     poly = env ? atoi(env) : kDefaultPoly;
     if (poly < 0 || poly > 2) poly = kDefaultPoly;
+    env = getenv("STAR_K1_SEQ");
+    seq = env ? (atoi(env) != 0) : kDefaultSeq;
+    env = getenv("STAR_K1_FH");
+    fh = env ? (atoi(env) != 0) : kDefaultFH;
+    env = getenv("STAR_K1_ONEP");
+    onep = env ? (atoi(env) != 0) : kDefaultOnePass;
   }
-  auto kern = poly == 0 ? phase1_tc_kernel<D, NQ, 0>
-                        : (poly == 1 ? phase1_tc_kernel<D, NQ, 1> : phase1_tc_kernel<D, NQ, 2>);
+  prm.seq = seq;
+  using KernFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, P1Params);
+  static const KernFn table[2][2][3] = {
+      {{phase1_tc_kernel<D, NQ, 0, false, false>, phase1_tc_kernel<D, NQ, 1, false, false>,
+        phase1_tc_kernel<D, NQ, 2, false, false>},
+       {phase1_tc_kernel<D, NQ, 0, true, false>, phase1_tc_kernel<D, NQ, 1, true, false>,
+        phase1_tc_kernel<D, NQ, 2, true, false>}},
+      {{phase1_tc_kernel<D, NQ, 0, false, true>, phase1_tc_kernel<D, NQ, 1, false, true>,
+        phase1_tc_kernel<D, NQ, 2, false, true>},
+       {phase1_tc_kernel<D, NQ, 0, true, true>, phase1_tc_kernel<D, NQ, 1, true, true>,
+        phase1_tc_kernel<D, NQ, 2, true, true>}}};
+  const KernFn kern = table[onep][fh][poly];
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
   dim3 grid(tiles * hkv * (hq / hkv / NQ));
@@ -623,4 +797,16 @@ int debug_umma_gemm(const void* a, const void* b, float* c, int K, int mode, cud
   return STAR_OK;
 }
 
+#ifdef STAR_K1_TRACE
+int debug_k1_trace(long long* host, int n) {
+  const int cap = (int)(sizeof(g_k1_trace) / sizeof(long long));
+  if (n > cap) n = cap;
+  return cudaMemcpyFromSymbol(host, g_k1_trace, n * sizeof(long long)) == cudaSuccess ? n : -4;
+}
+#endif
+
 }  // namespace star
+
+#ifdef STAR_K1_TRACE
+extern "C" int star_debug_k1_trace(long long* host, int n) { return star::debug_k1_trace(host, n); }
+#endif

@@ -38,4 +38,5 @@ for _ in range(a.iters):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.iters
-print(f"POLY={os.environ.get('STAR_K1_POLY', 'default')} ms={ms:.2f} TFLOP/s={flops / ms / 1e9:.1f}")
+knobs = " ".join(f"{k}={os.environ[k]}" for k in sorted(os.environ) if k.startswith("STAR_K1_"))
+print(f"{knobs or 'defaults'} ms={ms:.2f} TFLOP/s={flops / ms / 1e9:.1f}")
