@@ -360,17 +360,18 @@ def run_ours(args):
     torch.cuda.empty_cache()
     qd = ops.prng_fill((1, 1, hq, d), seed ^ 4, 1, 1.0, torch.bfloat16, dev)
     kv_len = torch.tensor([own_rows], dtype=torch.int32, device=dev)
-    gathered_o = torch.empty((world, hq, d), dtype=torch.float32, device=dev)
-    gathered_l = torch.empty((world, hq), dtype=torch.float32, device=dev)
+    # K2 writes (out, lse) straight into the packed wire format [hq*d | hq] of the single
+    # all-gather; K3 merges the gathered parts in place
+    packed, po, pl = ops.packed_partial(hq, d, dev)
+    gathered = torch.empty(world * hq * (d + 1), dtype=torch.float32, device=dev)
     ws = ops.Phase2Workspace()
 
     def decode_step():
         o, l = ops.phase2_partial(qd, kpool, vpool, table.view(1, -1), kv_len, own_rows,
-                                  workspace=ws)
+                                  out=po.view(1, 1, hq, d), lse=pl.view(1, 1, hq), workspace=ws)
         if world > 1:
-            dist.all_gather_into_tensor(gathered_o, o.view(1, hq, d))
-            dist.all_gather_into_tensor(gathered_l, l.view(1, hq))
-            return ops.merge(gathered_o, gathered_l)
+            dist.all_gather_into_tensor(gathered, packed)
+            return ops.merge_packed(gathered.view(world, -1), hq, d)
         return o, l
 
     # capture the per-token decode (K2 [+ all-gather + K3]) in a CUDA graph: a decode loop is
@@ -434,7 +435,7 @@ def run_ours(args):
                      "frac": kv_bytes / (k2_us * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6532.9),
                      "bytes_per_launch": kv_bytes,
                      "note": "K2 split-KV partial + in-GPU split merge; bytes = local KV rows x 8 heads x 128 x 2 (K,V) x 2 B"},
-        "collective": "NCCL all_gather of fp32 (out, lse)" if world > 1 else "none (1 rank)",
+        "collective": "one NCCL all_gather of packed fp32 (out | lse), hq*(d+1) per rank" if world > 1 else "none (1 rank)",
     }
 
     if rank != 0:

@@ -172,6 +172,15 @@ int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, i
 int star_merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d,
                void* out, int out_dtype, float* lse, void* stream);
 
+/* K3 over strided parts: part p's out rows start at outs + p * out_part_stride and its lse
+ * at lses + p * lse_part_stride (elements).  Used on the all-gathered packed partials
+ * [out rows*d | lse rows] of every rank, so one collective carries both (see dist.py).
+ * Replaces merge_partials (ss/attention.py:154-173) as _gather_merge calls it over the
+ * hosts in ascending order (ss/sim.py:190-213). */
+int star_merge_strided(const float* outs, int64_t out_part_stride, const float* lses,
+                       int64_t lse_part_stride, int n_parts, int64_t rows, int d, void* out,
+                       int out_dtype, float* lse, void* stream);
+
 /* Debug/validation: C[128x128] fp32 = A[128xK] * B^T via one tcgen05 CTA.
  * mode bit 0: B given MN-major as [K x 128]; bit 1: A staged through TMEM.
  * K multiple of 64. */

@@ -45,6 +45,8 @@ SIGNATURES = {
                                     c_int64, c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     "star_merge": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int, c_void_p, c_int, c_void_p,
                            c_void_p]),
+    "star_merge_strided": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int, c_int64, c_int,
+                                   c_void_p, c_int, c_void_p, c_void_p]),
     "star_debug_umma_gemm": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
 }
 

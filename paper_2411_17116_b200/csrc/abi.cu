@@ -71,6 +71,8 @@ int phase2_partial(const void*, int, int, int, int, int, int, const void*, const
                    int64_t, const int32_t*, int, int, const int32_t*, int64_t, int, float*, float*,
                    int, void*, cudaStream_t);
 int merge(const float*, const float*, int, int64_t, int, void*, int, float*, cudaStream_t);
+int merge_strided(const float*, int64_t, const float*, int64_t, int, int64_t, int, void*, int, float*,
+                  cudaStream_t);
 int debug_umma_gemm(const void*, const void*, float*, int, int, cudaStream_t);
 
 static int check_heads(int hq, int hkv, int d) {
@@ -234,6 +236,13 @@ int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, i
 int star_merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d, void* out,
                int out_dtype, float* lse, void* stream) {
   return merge(outs, lses, n_parts, rows, d, out, out_dtype, lse, (cudaStream_t)stream);
+}
+
+int star_merge_strided(const float* outs, int64_t out_part_stride, const float* lses,
+                       int64_t lse_part_stride, int n_parts, int64_t rows, int d, void* out,
+                       int out_dtype, float* lse, void* stream) {
+  return merge_strided(outs, out_part_stride, lses, lse_part_stride, n_parts, rows, d, out,
+                       out_dtype, lse, (cudaStream_t)stream);
 }
 
 int star_debug_umma_gemm(const void* a, const void* b, float* c, int K, int mode, void* stream) {

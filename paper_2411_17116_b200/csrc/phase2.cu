@@ -281,20 +281,21 @@ constexpr int kMergeMaxParts = 512;
 
 template <typename TO>
 __global__ void __launch_bounds__(kMergeWarps * 32) merge_kernel(
-    const float* __restrict__ outs, const float* __restrict__ lses, int n_parts, int64_t rows,
-    int d, TO* __restrict__ out, float* __restrict__ lse) {
+    const float* __restrict__ outs, int64_t out_pstride, const float* __restrict__ lses,
+    int64_t lse_pstride, int n_parts, int64_t rows, int d, TO* __restrict__ out,
+    float* __restrict__ lse) {
   __shared__ float wsm[kMergeWarps][kMergeMaxParts];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * (int64_t)kMergeWarps + warp;
   if (row >= rows) return;
   float* w = wsm[warp];
   double mx = -INFINITY;
-  for (int p = lane; p < n_parts; p += 32) mx = fmax(mx, (double)lses[(int64_t)p * rows + row]);
+  for (int p = lane; p < n_parts; p += 32) mx = fmax(mx, (double)lses[(int64_t)p * lse_pstride + row]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   double acc = 0.0;
   for (int p = lane; p < n_parts; p += 32) {
-    const double l = lses[(int64_t)p * rows + row];
+    const double l = lses[(int64_t)p * lse_pstride + row];
     const double e = (l == -INFINITY) ? 0.0 : exp(l - mx);
     w[p] = (float)e;
     acc += e;
@@ -306,28 +307,37 @@ __global__ void __launch_bounds__(kMergeWarps * 32) merge_kernel(
   __syncwarp();
   for (int c = lane; c < d; c += 32) {
     float o = 0.f;
-    for (int p = 0; p < n_parts; ++p) o = fmaf(w[p], outs[((int64_t)p * rows + row) * d + c], o);
+    for (int p = 0; p < n_parts; ++p) o = fmaf(w[p], outs[(int64_t)p * out_pstride + row * d + c], o);
     out[row * d + c] = Elem<TO>::from_f(o * inv);
   }
   if (lse != nullptr && lane == 0) lse[row] = (float)s;
 }
 
-int merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d, void* out,
-          int out_dtype, float* lse, cudaStream_t s) {
+int merge_strided(const float* outs, int64_t out_pstride, const float* lses, int64_t lse_pstride,
+                  int n_parts, int64_t rows, int d, void* out, int out_dtype, float* lse,
+                  cudaStream_t s) {
   if (n_parts < 1) return fail(STAR_EDOMAIN, "merge of zero partials");
   if (n_parts > kMergeMaxParts) return fail(STAR_ENOTSUP, "merge of more than %d partials", kMergeMaxParts);
   if (rows < 0 || d < 1) return fail(STAR_ESHAPE, "merge: bad shape");
+  if (out_pstride < rows * d || lse_pstride < rows)
+    return fail(STAR_ESHAPE, "merge: part strides smaller than a part");
   if (rows == 0) return STAR_OK;
   int grid = (int)((rows + kMergeWarps - 1) / kMergeWarps);
   if (out_dtype == STAR_F32)
-    merge_kernel<float><<<grid, kMergeWarps * 32, 0, s>>>(outs, lses, n_parts, rows, d, (float*)out, lse);
+    merge_kernel<float><<<grid, kMergeWarps * 32, 0, s>>>(outs, out_pstride, lses, lse_pstride,
+                                                          n_parts, rows, d, (float*)out, lse);
   else if (out_dtype == STAR_BF16)
-    merge_kernel<__nv_bfloat16><<<grid, kMergeWarps * 32, 0, s>>>(outs, lses, n_parts, rows, d,
-                                                     (__nv_bfloat16*)out, lse);
+    merge_kernel<__nv_bfloat16><<<grid, kMergeWarps * 32, 0, s>>>(
+        outs, out_pstride, lses, lse_pstride, n_parts, rows, d, (__nv_bfloat16*)out, lse);
   else
     return fail(STAR_ECONFIG, "merge: unknown dtype %d", out_dtype);
   STAR_LAUNCH_CHECK("merge");
   return STAR_OK;
+}
+
+int merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d, void* out,
+          int out_dtype, float* lse, cudaStream_t s) {
+  return merge_strided(outs, rows * d, lses, rows, n_parts, rows, d, out, out_dtype, lse, s);
 }
 
 // ------------------------------------------------------------------ host side
@@ -419,7 +429,8 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
   if (kv_dtype == STAR_BF16 && n_splits > 1) {
     // the in-kernel split fix-up stages n_splits x QR weights in the idle TMA ring
     const int64_t qr = (int64_t)(hq / hkv) * lq;
-    const int64_t cap = ((d == 128 ? 6 * 32768 : 6 * 16384) - 64) / (4 * qr) - 1;
+    // (and the fix-up folds at most 256 splits)
+    const int64_t cap = std::min<int64_t>(256, ((d == 128 ? 6 * 32768 : 6 * 16384) - 64) / (4 * qr) - 1);
     if (n_splits > cap) {
       n_splits = (int)std::max<int64_t>(1, cap);
       chunk = (max_kv_len + n_splits - 1) / n_splits;

@@ -14,6 +14,7 @@
 //   row mode (G*lq > 16, query encode): warp w takes q rows [16w, 16w+16) of a
 //     64-row pass over every key of the tile.
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -66,9 +67,12 @@ __device__ __forceinline__ uint32_t swz(uint32_t slab, int row, int chunk) {
 
 }  // namespace p2
 
-// Serial split-K fix-up: the last CTA of a (sequence, kv head) to finish folds the
-// gridDim.x split partials (still L2-resident) with the merge rule, in ascending split
-// order, and re-arms the counter.  Consumer threads only (128; the producer has exited).
+// Split-K fix-up: the last CTA of a (sequence, kv head) to finish folds the gridDim.x
+// split partials (still L2-resident) with the merge rule, in ascending split order, and
+// re-arms the counter.  Consumer threads only (128; the producer has exited).  This tail
+// is serial latency after the last split lands, so every step keeps many independent
+// L2 loads in flight: the lse of all splits in one round, the out partials 8 splits x 4
+// elements per thread per round.
 template <int D>
 __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq, int G,
                             const float* ws_out, const float* ws_lse, int64_t part_rows,
@@ -79,53 +83,78 @@ __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq,
   const int nsp = gridDim.x;
   const int QR = G * lq;
   int* flag = reinterpret_cast<int*>(smem);
-  __threadfence();
-  named_barrier_sync(1, NT);
+  named_barrier_sync(1, NT);  // every consumer's partial stores precede thread 0's release
   if (tid == 0) {
+    __threadfence();
     const int old = atomicAdd(&counters[b * gridDim.y + kvh], 1);
+    __threadfence();
     *flag = (old == nsp - 1);
   }
   named_barrier_sync(1, NT);
   if (!*flag) return;
-  __threadfence();
-  float* w = reinterpret_cast<float*>(smem + 16);  // [nsp][QR] weights
-  float* srow = w + nsp * QR;                       // [QR] merged lse
+  float* w = reinterpret_cast<float*>(smem + 16);  // [nsp][QR] normalised merge weights
   const int warp = tid >> 5, lane = tid & 31;
   for (int rr = warp; rr < QR; rr += NT / 32) {
     const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
+    float lv[8];  // splits lane + 32 u (nsp <= 256)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = lane + 32 * u;
+      lv[u] = p < nsp ? __ldcg(ws_lse + p * part_rows + orow) : -INFINITY;
+    }
     float m = -INFINITY;
-    for (int p = lane; p < nsp; p += 32) m = fmaxf(m, ws_lse[p * part_rows + orow]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m = fmaxf(m, lv[u]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     float acc = 0.f;
-    for (int p = lane; p < nsp; p += 32) {
-      const float l = ws_lse[p * part_rows + orow];
-      const float e = (l == -INFINITY) ? 0.f : __expf(l - m);
-      w[p * QR + rr] = e;
-      acc += e;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      lv[u] = (lv[u] == -INFINITY) ? 0.f : __expf(lv[u] - m);
+      acc += lv[u];
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     const float inv = acc > 0.f ? 1.f / acc : 0.f;
-    for (int p = lane; p < nsp; p += 32) w[p * QR + rr] *= inv;
-    if (lane == 0) {
-      const float sl = acc > 0.f ? m + __logf(acc) : -INFINITY;
-      srow[rr] = sl;
-      final_lse[orow] = sl;
-    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (lane + 32 * u < nsp) w[(lane + 32 * u) * QR + rr] = lv[u] * inv;
+    if (lane == 0) final_lse[orow] = acc > 0.f ? m + __logf(acc) : -INFINITY;
   }
   named_barrier_sync(1, NT);
-  for (int e = tid; e < QR * D; e += NT) {
-    const int rr = e / D, c = e % D;
-    const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
-    float acc = 0.f;
-    for (int p = 0; p < nsp; ++p) acc = fmaf(w[p * QR + rr], ws_out[(p * part_rows + orow) * D + c], acc);
-    final_out[orow * D + c] = acc;
+  for (int e0 = tid; e0 < QR * D; e0 += 4 * NT) {
+    int rr[4], c[4];
+    int64_t orow[4];
+    float acc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = min(e0 + k * NT, QR * D - 1);
+      rr[k] = e / D;
+      c[k] = e % D;
+      orow[k] = ((int64_t)b * lq + rr[k] / G) * hq + kvh * G + rr[k] % G;
+      acc[k] = 0.f;
+    }
+    for (int p0 = 0; p0 < nsp; p0 += 8) {
+      float v[8][4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          v[u][k] = p0 + u < nsp ? __ldcg(ws_out + ((p0 + u) * part_rows + orow[k]) * D + c[k]) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (p0 + u < nsp) acc[k] = fmaf(w[(p0 + u) * QR + rr[k]], v[u][k], acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (e0 + k * NT < QR * D) final_out[orow[k] * D + c[k]] = acc[k];
   }
   if (tid == 0) counters[b * gridDim.y + kvh] = 0;  // re-arm for the next launch
 }
 
-template <int D, bool KEYSPLIT>
+template <int D, bool KEYSPLIT, bool PLO>
 __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
     const __nv_bfloat16* __restrict__ q, int lq, int hq, int hkv,
@@ -167,25 +196,42 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
 
   if (warp == kConsumers) {
     // ================= TMA producer =================
+    // The whole warp resolves page-table entries 32 tiles at a time (lane l -> tile t0+l,
+    // one coalesced load, the next group's load in flight while this group is issued);
+    // lane 0 then issues the TMA loads back to back, so the ring fills without a
+    // dependent table read in front of every tile.
     if (lane == 0) {
       tma_prefetch(&tm_k);
       tma_prefetch(&tm_v);
-      int it = 0;
-      for (int pass = 0; pass < n_pass; ++pass) {
-        for (int t = 0; t < ntiles; ++t, ++it) {
-          const int st = it % STAGES;
-          if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) + 1) & 1);
-          const int64_t row = r0 + (int64_t)t * TN;
-          const int64_t page = table[row / page_size];
-          const int prow = (int)((page * hkv + kvh) * page_size + row % page_size);
-          unsigned char* kb = smem + st * SM::kStage;
-          mbar_expect_tx(&full[st], SM::kStage);
+    }
+    auto page_row = [&](int t) -> int {
+      if (t >= ntiles) return 0;
+      const int64_t row = r0 + (int64_t)t * TN;
+      const int64_t page = table[row / page_size];
+      return (int)((page * hkv + kvh) * page_size + row % page_size);
+    };
+    int it = 0;
+    for (int pass = 0; pass < n_pass; ++pass) {
+      int cur = page_row(lane);
+      for (int t0 = 0; t0 < ntiles; t0 += 32) {
+        const int nxt = page_row(t0 + 32 + lane);
+        const int cnt = min(32, ntiles - t0);
+        for (int u = 0; u < cnt; ++u, ++it) {
+          const int prow = __shfl_sync(0xffffffffu, cur, u);
+          if (lane == 0) {
+            const int st = it % STAGES;
+            if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) + 1) & 1);
+            unsigned char* kb = smem + st * SM::kStage;
+            mbar_expect_tx(&full[st], SM::kStage);
 #pragma unroll
-          for (int a = 0; a < D / 64; ++a) {
-            tma_load_2d(kb + a * SM::kSlab, &tm_k, &full[st], a * 64, prow);
-            tma_load_2d(kb + SM::kTile + a * SM::kSlab, &tm_v, &full[st], a * 64, prow);
+            for (int a = 0; a < D / 64; ++a) {
+              tma_load_2d(kb + a * SM::kSlab, &tm_k, &full[st], a * 64, prow);
+              tma_load_2d(kb + SM::kTile + a * SM::kSlab, &tm_v, &full[st], a * 64, prow);
+            }
           }
+          __syncwarp();
         }
+        cur = nxt;
       }
     }
     return;
@@ -301,12 +347,18 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
       for (int n = 0; n < NT_K; ++n) {
         const float p0 = ex2(sc[n][0] - uA), p1 = ex2(sc[n][1] - uA);
         const float p2v = ex2(sc[n][2] - uB), p3 = ex2(sc[n][3] - uB);
-        sA += p0 + p1;
-        sB += p2v + p3;
         pa[n][0] = pack_bf16x2(p0, p1);
         pa[n][1] = pack_bf16x2(p2v, p3);
-        pl[n][0] = pack_bf16x2(p0 - bf16lo(pa[n][0]), p1 - bf16hi(pa[n][0]));
-        pl[n][1] = pack_bf16x2(p2v - bf16lo(pa[n][1]), p3 - bf16hi(pa[n][1]));
+        if (PLO) {
+          sA += p0 + p1;
+          sB += p2v + p3;
+          pl[n][0] = pack_bf16x2(p0 - bf16lo(pa[n][0]), p1 - bf16hi(pa[n][0]));
+          pl[n][1] = pack_bf16x2(p2v - bf16lo(pa[n][1]), p3 - bf16hi(pa[n][1]));
+        } else {
+          // bf16 P only: the row sum takes the same rounded weights as the P.V product
+          sA += bf16lo(pa[n][0]) + bf16hi(pa[n][0]);
+          sB += bf16lo(pa[n][1]) + bf16hi(pa[n][1]);
+        }
       }
       lA = lA * aA + sA;
       lB = lB * aB + sB;
@@ -325,7 +377,13 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
 #pragma unroll
       for (int kk = 0; kk < KW / 16; ++kk) {
         const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
-        const uint32_t al[4] = {pl[2 * kk][0], pl[2 * kk][1], pl[2 * kk + 1][0], pl[2 * kk + 1][1]};
+        uint32_t al[4] = {0u, 0u, 0u, 0u};
+        if (PLO) {
+          al[0] = pl[2 * kk][0];
+          al[1] = pl[2 * kk][1];
+          al[2] = pl[2 * kk + 1][0];
+          al[3] = pl[2 * kk + 1][1];
+        }
         const int vrow = kofs + kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
 #pragma unroll
         for (int nd = 0; nd < NT_D; nd += 2) {
@@ -336,8 +394,10 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
           ldsm_x4_t(addr, b0, b1, b2, b3);
           mma16816(o[nd], a, b0, b1);
           mma16816(o[nd + 1], a, b2, b3);
-          mma16816(o[nd], al, b0, b1);
-          mma16816(o[nd + 1], al, b2, b3);
+          if (PLO) {
+            mma16816(o[nd], al, b0, b1);
+            mma16816(o[nd + 1], al, b2, b3);
+          }
         }
       }
       fence_proxy_async_smem();  // generic-proxy zeroing above vs the next TMA write
@@ -410,7 +470,7 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
       }
     }
   }
-  if (gridDim.x > 1) split_fixup<D>(smem, b, kvh, lq, hq, G, out, lse, part_stride_rows, final_out,
+  if (gridDim.x > 1 && counters != nullptr) split_fixup<D>(smem, b, kvh, lq, hq, G, out, lse, part_stride_rows, final_out,
                                     final_lse, counters);
 }
 
@@ -445,11 +505,16 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     return fail(STAR_ECONFIG, "phase2: %d splits x %d query rows exceed the fix-up buffer", n_splits,
                 QR);
   dim3 grid(n_splits, hkv, batch);
+  // timing experiment only (tools/decode_bench.py): skip the split fix-up (result incomplete)
+  static const bool no_fix = getenv("STAR_K2_EXPERIMENT_NOFIX") != nullptr;
+  if (no_fix) counters = nullptr;
+  // P.V precision: bf16 hi + lo split of P (1, default) or bf16 P with matching row sums (0)
+  static const bool plo = getenv("STAR_K2_PLO") == nullptr || atoi(getenv("STAR_K2_PLO")) != 0;
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)d));
   const int64_t part_rows = (int64_t)batch * lq * hq;
 #define STAR_P2M(DD, KS)                                                                        \
   do {                                                                                          \
-    auto kern = phase2_mma_kernel<DD, KS>;                                                      \
+    auto kern = plo ? phase2_mma_kernel<DD, KS, true> : phase2_mma_kernel<DD, KS, false>;       \
     const int bytes = Smem<DD>::kBytes;                                                         \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \

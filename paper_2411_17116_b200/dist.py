@@ -80,21 +80,41 @@ def rank_shard(plan: BlockPlan, blocks_aug, rank: int) -> RankShard:
     return RankShard(rank, tuple(mine), tuple(seg), tuple(lo), tuple(c0), tuple(pos), tuple(cpos))
 
 
-def gather_partials(out: torch.Tensor, lse: torch.Tensor, group=None):
-    """All-gather one partial per rank: out [rows, d] fp32, lse [rows] -> [world, rows, d], [world, rows]."""
+def gather_packed(packed: torch.Tensor, group=None) -> torch.Tensor:
+    """ONE all-gather of every rank's packed partial [rows*d out | rows lse] -> [world, rows*(d+1)]."""
     world = dist.get_world_size(group)
-    rows = out.shape[0]
-    outs = torch.empty((world * rows,) + tuple(out.shape[1:]), dtype=out.dtype, device=out.device)
-    lses = torch.empty((world * rows,), dtype=lse.dtype, device=lse.device)
-    dist.all_gather_into_tensor(outs, out.contiguous(), group=group)
-    dist.all_gather_into_tensor(lses, lse.contiguous().view(-1), group=group)
-    return outs.view((world,) + tuple(out.shape)), lses.view(world, rows)
+    parts = torch.empty(world * packed.numel(), dtype=packed.dtype, device=packed.device)
+    dist.all_gather_into_tensor(parts, packed.contiguous().view(-1), group=group)
+    return parts.view(world, packed.numel())
+
+
+def gather_partials(out: torch.Tensor, lse: torch.Tensor, group=None):
+    """All-gather one partial per rank: out [rows, d] fp32, lse [rows] -> [world, rows, d], [world, rows].
+
+    Both travel in one packed collective (the wire format of SURVEY §8e: l_q*Hq*(d+1) fp32
+    per rank)."""
+    rows, d = out.shape[0], out[0].numel()
+    packed = torch.cat([out.reshape(-1), lse.reshape(-1)])
+    parts = gather_packed(packed, group)
+    world = parts.shape[0]
+    return (parts[:, :rows * d].reshape((world,) + tuple(out.shape)),
+            parts[:, rows * d:].reshape(world, rows))
 
 
 def gather_merge(out: torch.Tensor, lse: torch.Tensor, merge_fn: Callable | None = None,
-                 group=None):
+                 group=None, packed: torch.Tensor | None = None):
     """All-gather the ranks' partials and fold them in ascending rank order (ranks whose
-    cache is empty contribute lse = -inf and are skipped, ss/sim.py:193-194)."""
+    cache is empty contribute lse = -inf and are skipped, ss/sim.py:193-194).
+
+    `packed`, when given, is the buffer `out`/`lse` are views of (ops.packed_partial): the
+    collective then sends it as is and K3 reads the gathered parts in place."""
+    if merge_fn is None and out.is_cuda:
+        from . import ops
+
+        rows, d = out.shape[0], out[0].numel()
+        if packed is None:
+            packed = torch.cat([out.reshape(-1), lse.reshape(-1)])
+        return ops.merge_packed(gather_packed(packed, group), rows, d)
     outs, lses = gather_partials(out, lse, group)
     if merge_fn is None:
         from . import ops
@@ -176,21 +196,22 @@ def _phase2_forward_dist(sess: DistSession, token_ids, positions, own_tail: int,
             sess.pool.append(li, k, v, pos)
         l = q.shape[0]
         n = sess.pool.rows(li)
+        packed, o, s = ops.packed_partial(l * H, hd, q.device)
         if n:
-            o, s = ops.phase2_partial(q.view(1, l, H, hd).to(sess.pool.dtype).contiguous(),
-                                      sess.pool.k[li], sess.pool.v[li],
-                                      sess.pool.page_table.view(1, -1), sess.pool.kv_len_tensor(li),
-                                      n, own_tail=own_tail if rank == sess.q_rank else 0)
-            o, s = o.view(l * H, hd), s.view(l * H)
+            ops.phase2_partial(q.view(1, l, H, hd).to(sess.pool.dtype).contiguous(),
+                               sess.pool.k[li], sess.pool.v[li],
+                               sess.pool.page_table.view(1, -1), sess.pool.kv_len_tensor(li),
+                               n, own_tail=own_tail if rank == sess.q_rank else 0,
+                               out=o.view(1, l, H, hd), lse=s.view(1, l, H))
         else:
-            o = torch.zeros((l * H, hd), dtype=torch.float32, device=q.device)
-            s = torch.full((l * H,), float("-inf"), dtype=torch.float32, device=q.device)
+            o.zero_()
+            s.fill_(float("-inf"))
         if nonempty is None:
             flags = torch.tensor([1 if n else 0], device=q.device)
             allf = torch.empty(world, dtype=flags.dtype, device=q.device)
             dist.all_gather_into_tensor(allf, flags, group=group)
             nonempty = [r for r in range(world) if int(allf[r])]
-        att, _ = gather_merge(o, s, group=group)
+        att, _ = gather_merge(o, s, group=group, packed=packed)
         x = finish_layer(x, att.view(l, H, hd), lw)
     if rank == sess.q_rank:
         sess.ledger.extend(phase2_ledger_rows(sess.q_rank, nonempty, cfg.layers, H, len(pos), hd))

@@ -281,6 +281,30 @@ def merge(outs: torch.Tensor, lses: torch.Tensor, out_dtype=torch.float32):
     return out, lse
 
 
+def packed_partial(rows: int, d: int, device) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """One fp32 buffer [rows*d out | rows lse] plus (out, lse) views into it: K2 writes its
+    partial straight into the wire format of the single all-gather (dist.gather_merge)."""
+    buf = torch.empty(rows * (d + 1), dtype=torch.float32, device=device)
+    return buf, buf[:rows * d].view(rows, d), buf[rows * d:]
+
+
+def merge_packed(parts: torch.Tensor, rows: int, d: int, out_dtype=torch.float32):
+    """K3 over all-gathered packed partials parts [P, rows*(d+1)] (ascending part order)."""
+    _cuda(parts)
+    if parts.dtype != torch.float32:
+        raise ConfigError("partials must be fp32")
+    if parts.dim() != 2 or parts.shape[1] != rows * (d + 1):
+        raise ShapeError("packed partials must be [P, rows*(d+1)]")
+    parts = parts.contiguous()
+    P = parts.shape[0]
+    out = torch.empty((rows, d), dtype=out_dtype, device=parts.device)
+    lse = torch.empty((rows,), dtype=torch.float32, device=parts.device)
+    base = parts.data_ptr()
+    _lib.call("star_merge_strided", base, rows * (d + 1), base + rows * d * 4, rows * (d + 1), P,
+              rows, d, out.data_ptr(), _DT[out_dtype], lse.data_ptr(), _stream(parts.device))
+    return out, lse
+
+
 def debug_umma_gemm(a: torch.Tensor, b: torch.Tensor, b_mn_major: bool = False,
                     a_tmem: bool = False) -> torch.Tensor:
     """C = A . B^T on one tcgen05 CTA (descriptor self-test); a [128, K], b [128, K] or [K, 128]."""

@@ -239,6 +239,14 @@ def test_merge_matches_reference(ops, golden_dir):
     outs2 = torch.cat([outs, torch.full_like(outs[:1], 123.0)])
     out2, lse2 = ops.merge(outs2, lses2)
     assert torch.allclose(out2, out) and torch.allclose(lse2, lse)
+    # the packed wire format of the single all-gather ([rows*d out | rows lse] per part)
+    # merges bit-identically to the separate tensors
+    P, rows, d = outs.shape
+    packed = torch.cat([outs.reshape(P, -1), lses.reshape(P, -1)], dim=1).contiguous()
+    out3, lse3 = ops.merge_packed(packed, rows, d)
+    assert torch.equal(out3, out) and torch.equal(lse3, lse)
+    buf, po, pl = ops.packed_partial(rows, d, outs.device)
+    assert po.data_ptr() == buf.data_ptr() and pl.data_ptr() == buf.data_ptr() + rows * d * 4
 
 
 def test_phase1_anchor_dedup_bit_exact(ops):

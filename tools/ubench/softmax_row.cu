@@ -57,7 +57,9 @@ __global__ void kern(float* out, int iters, long long* cyc) {
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {
         float2 x = ffma2(make_float2(sv[c * 32 + e], sv[c * 32 + e + 1]), sc2, nm2);
-        if (MODE >= 2 && c >= 6 - MODE) {  // MODE 2: chunk 3 on FMA; MODE 3: chunks 2-3
+        const bool poly = MODE == 2 || MODE == 3 ? c >= 6 - MODE
+                        : MODE == 4 ? ((e >> 1) & 3) == 3 : MODE == 5 ? ((e >> 1) & 7) == 7 : false;
+        if (poly) {  // MODE 2: chunk 3 on FMA; 3: chunks 2-3; 4: every 4th pair; 5: every 8th
           float2 q = poly_ex2x2(x);
           p[e] = q.x;
           p[e + 1] = q.y;
@@ -83,14 +85,15 @@ __global__ void kern(float* out, int iters, long long* cyc) {
 int main() {
   float* out; long long* cyc; cudaMalloc(&out, 148 * 1024 * 4); cudaMalloc(&cyc, 8);
   const int iters = 2048;
-  for (int mode = 0; mode < 4; ++mode)
+  for (int mode = 0; mode < 6; ++mode)
     for (int wps = 1; wps <= 3; ++wps) {
-      auto k = mode == 0 ? kern<0> : mode == 1 ? kern<1> : mode == 2 ? kern<2> : kern<3>;
+      auto k = mode == 0 ? kern<0> : mode == 1 ? kern<1> : mode == 2 ? kern<2> : mode == 3 ? kern<3>
+             : mode == 4 ? kern<4> : kern<5>;
       k<<<148, 128 * wps>>>(out, 8, cyc);
       k<<<148, 128 * wps>>>(out, iters, cyc);
       long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
       printf("mode=%s warps/SMSP=%d: %.1f clk per 128-score row per warp (MUFU floor 1024 x warps)\n",
-             mode == 0 ? "exp+pack" : mode == 1 ? "exp+pack+sum" : mode == 2 ? "+sum, 1/4 poly" : "+sum, 1/2 poly", wps, (double)c / iters);
+             mode == 0 ? "exp+pack" : mode == 1 ? "exp+pack+sum" : mode == 2 ? "+sum, 1/4 poly" : mode == 3 ? "+sum, 1/2 poly" : mode == 4 ? "+sum, 1/4 poly spread" : "+sum, 1/8 poly spread", wps, (double)c / iters);
     }
   return 0;
 }
