@@ -444,6 +444,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return 0
 
+    sweep = None if args.no_sweep else decode_sweep(dev, hq, hkv, d, peaks.get("hbm_gbs", 6532.9))
     cpu = None
     if not args.no_cpu_baseline:
         t, rows, reps = cpu_sample(budget_s=12.0)
@@ -469,6 +470,7 @@ def run_ours(args):
                      "flops_per_launch": flops, "kernel_ms": k1_ms,
                      "flops_def": "star pairs x Hq x 4 x d (anchor query rows included)"},
         "decode": decode,
+        "decode_sweep": sweep,
         "anchor_dedup": dedup_info,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -482,6 +484,49 @@ def run_ours(args):
     return 0
 
 
+def decode_sweep(dev, hq, hkv, d, hbm_peak):
+    """BASELINE configs[4] on one GPU: K2 per-token latency per layer over batch x cached
+    tokens (one layer's paged cache; B x S beyond HBM for 32 layers)."""
+    import torch
+
+    from paper_2411_17116_b200 import ops
+
+    out = []
+    for B, S in ((1, 32768), (1, 131072), (1, 1048576), (8, 131072), (32, 32768)):
+        page = 128
+        pages = B * (S // page)
+        kp = ops.prng_fill((pages, hkv, page, d), 21, 1, 1.0, torch.bfloat16, dev)
+        vp = ops.prng_fill((pages, hkv, page, d), 22, 1, 1.0, torch.bfloat16, dev)
+        table = torch.arange(pages, dtype=torch.int32, device=dev).view(B, -1)
+        q = ops.prng_fill((B, 1, hq, d), 23, 1, 1.0, torch.bfloat16, dev)
+        kv_len = torch.full((B,), S, dtype=torch.int32, device=dev)
+        ws = ops.Phase2Workspace()
+        f = lambda: ops.phase2_partial(q, kp, vp, table, kv_len, S, workspace=ws)  # noqa: E731
+        f()
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+            for _ in range(10):
+                f()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        us = e0.elapsed_time(e1) / 50 * 1e3
+        nbytes = B * S * hkv * d * 2 * 2
+        out.append({"batch": B, "cached_tokens": S, "us_per_token_per_layer": us,
+                    "gbs": nbytes / us / 1e3, "frac_of_measured_hbm": nbytes / us / 1e3 / hbm_peak})
+        del kp, vp, g
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -490,6 +535,7 @@ def main():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-sweep", action="store_true")
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3

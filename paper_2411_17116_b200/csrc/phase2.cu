@@ -356,6 +356,9 @@ int phase2_auto_splits(int batch, int hkv, int64_t max_kv_len, int page_size) {
   // one wave: about one CTA per SM (the bf16 path keeps 128 KB of TMA stages per CTA);
   // at least 256 keys per split
   int64_t want = (int64_t)num_sms() / std::max(1, batch * hkv);
+  // 16 splits (one DSMEM-merged cluster per sequence x kv head) when that still covers
+  // most SMs: measured faster than a full 18-split wave with the global fix-up
+  if (want > 16 && (int64_t)batch * hkv * 16 * 5 >= (int64_t)num_sms() * 4) want = 16;
   int64_t max_by_len = std::max<int64_t>(1, max_kv_len / 256);
   int64_t s = std::max<int64_t>(1, std::min(want, max_by_len));
   return (int)std::min<int64_t>(s, 256);

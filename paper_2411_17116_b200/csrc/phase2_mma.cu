@@ -27,8 +27,15 @@ namespace p2 {
 
 constexpr int TN = 64;       // keys per tile (must divide page_size)
 constexpr int STAGES = 6;
-constexpr int kConsumers = 4;
-constexpr int kThreads = (kConsumers + 1) * 32;
+// consumer warps: decode (KEYSPLIT) runs two groups of four that take alternate tiles, so
+// every SM sub-partition has two independent mma.sync chains in flight; the query-encode
+// row mode runs one group of four
+template <bool KEYSPLIT>
+struct Cons {
+  static constexpr int NC = KEYSPLIT ? 8 : 4;   // consumer warps
+  static constexpr int NG = NC / 4;             // tile groups
+  static constexpr int kThreads = (NC + 1) * 32;
+};
 
 template <int D>
 struct Smem {
@@ -68,17 +75,16 @@ __device__ __forceinline__ uint32_t swz(uint32_t slab, int row, int chunk) {
 }  // namespace p2
 
 // Split-K fix-up: the last CTA of a (sequence, kv head) to finish folds the gridDim.x
-// split partials (still L2-resident) with the merge rule, in ascending split order, and
-// re-arms the counter.  Consumer threads only (128; the producer has exited).  This tail
-// is serial latency after the last split lands, so every step keeps many independent
-// L2 loads in flight: the lse of all splits in one round, the out partials 8 splits x 4
-// elements per thread per round.
-template <int D>
+// split partials (still L2-resident) with the merge rule and re-arms the counter.
+// Consumer threads only (the producer has exited).  This tail is pure latency after the
+// last split lands, so it is one round of L2 loads: each thread takes two output elements
+// and loads the lse and out of 16 splits for both at once (64 loads in flight), folding
+// further groups of 16 splits, if any, online (running max, as the kernel's tile fold).
+template <int D, int NT>
 __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq, int G,
                             const float* ws_out, const float* ws_lse, int64_t part_rows,
                             float* final_out, float* final_lse, int* counters) {
-  using namespace p2;
-  constexpr int NT = kConsumers * 32;
+  constexpr int PS = 16;  // splits per load round
   const int tid = threadIdx.x;
   const int nsp = gridDim.x;
   const int QR = G * lq;
@@ -92,70 +98,59 @@ __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq,
   }
   named_barrier_sync(1, NT);
   if (!*flag) return;
-  float* w = reinterpret_cast<float*>(smem + 16);  // [nsp][QR] normalised merge weights
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int rr = warp; rr < QR; rr += NT / 32) {
-    const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
-    float lv[8];  // splits lane + 32 u (nsp <= 256)
+  for (int e0 = tid; e0 < QR * D; e0 += 2 * NT) {
+    int64_t orow[2];
+    int c[2];
+    bool ok[2];
+    float m[2] = {-INFINITY, -INFINITY}, acc[2] = {0.f, 0.f}, o[2] = {0.f, 0.f};
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int p = lane + 32 * u;
-      lv[u] = p < nsp ? __ldcg(ws_lse + p * part_rows + orow) : -INFINITY;
+    for (int k = 0; k < 2; ++k) {
+      const int e = e0 + k * NT;
+      ok[k] = e < QR * D;
+      const int rr = (ok[k] ? e : 0) / D;
+      c[k] = (ok[k] ? e : 0) % D;
+      orow[k] = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
     }
-    float m = -INFINITY;
+    for (int p0 = 0; p0 < nsp; p0 += PS) {
+      float lv[2][PS], ov[2][PS];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) m = fmaxf(m, lv[u]);
+      for (int k = 0; k < 2; ++k)
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float acc = 0.f;
+        for (int u = 0; u < PS; ++u) {
+          const bool in = ok[k] && p0 + u < nsp;
+          lv[k][u] = in ? __ldcg(ws_lse + (p0 + u) * part_rows + orow[k]) : -INFINITY;
+          ov[k][u] = in ? __ldcg(ws_out + ((p0 + u) * part_rows + orow[k]) * D + c[k]) : 0.f;
+        }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      lv[u] = (lv[u] == -INFINITY) ? 0.f : __expf(lv[u] - m);
-      acc += lv[u];
-    }
+      for (int k = 0; k < 2; ++k) {
+        float mn = m[k];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    const float inv = acc > 0.f ? 1.f / acc : 0.f;
+        for (int u = 0; u < PS; ++u) mn = fmaxf(mn, lv[k][u]);
+        if (mn == -INFINITY) continue;  // nothing visible yet (empty splits)
+        const float sc = __expf(m[k] - mn);  // 0 while m is -inf
+        acc[k] *= sc;
+        o[k] *= sc;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (lane + 32 * u < nsp) w[(lane + 32 * u) * QR + rr] = lv[u] * inv;
-    if (lane == 0) final_lse[orow] = acc > 0.f ? m + __logf(acc) : -INFINITY;
-  }
-  named_barrier_sync(1, NT);
-  for (int e0 = tid; e0 < QR * D; e0 += 4 * NT) {
-    int rr[4], c[4];
-    int64_t orow[4];
-    float acc[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int e = min(e0 + k * NT, QR * D - 1);
-      rr[k] = e / D;
-      c[k] = e % D;
-      orow[k] = ((int64_t)b * lq + rr[k] / G) * hq + kvh * G + rr[k] % G;
-      acc[k] = 0.f;
-    }
-    for (int p0 = 0; p0 < nsp; p0 += 8) {
-      float v[8][4];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          v[u][k] = p0 + u < nsp ? __ldcg(ws_out + ((p0 + u) * part_rows + orow[k]) * D + c[k]) : 0.f;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (p0 + u < nsp) acc[k] = fmaf(w[(p0 + u) * QR + rr[k]], v[u][k], acc[k]);
+        for (int u = 0; u < PS; ++u) {
+          const float w = lv[k][u] == -INFINITY ? 0.f : __expf(lv[k][u] - mn);
+          acc[k] += w;
+          o[k] = fmaf(w, ov[k][u], o[k]);
+        }
+        m[k] = mn;
+      }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (e0 + k * NT < QR * D) final_out[orow[k] * D + c[k]] = acc[k];
+    for (int k = 0; k < 2; ++k) {
+      if (!ok[k]) continue;
+      final_out[orow[k] * D + c[k]] = acc[k] > 0.f ? o[k] / acc[k] : 0.f;
+      if (c[k] == 0) final_lse[orow[k]] = acc[k] > 0.f ? m[k] + __logf(acc[k]) : -INFINITY;
+    }
   }
   if (tid == 0) counters[b * gridDim.y + kvh] = 0;  // re-arm for the next launch
 }
 
-template <int D, bool KEYSPLIT, bool PLO>
-__global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
+template <int D, bool KEYSPLIT>
+__global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kernel(
     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
     const __nv_bfloat16* __restrict__ q, int lq, int hq, int hkv,
     const int32_t* __restrict__ page_table, int pages_per_seq, int page_size,
@@ -164,6 +159,7 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
     float* __restrict__ final_out, float* __restrict__ final_lse, int* __restrict__ counters) {
   using namespace p2;
   using SM = Smem<D>;
+  constexpr int NC = Cons<KEYSPLIT>::NC, NG = Cons<KEYSPLIT>::NG;
   constexpr int NT_D = D / 8;  // n-tiles over head dim (P.V output)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -188,13 +184,13 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers);
+      mbar_init(&empty[s], 4);  // one group of four consumer warps per tile
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kConsumers) {
+  if (warp == NC) {
     // ================= TMA producer =================
     // The whole warp resolves page-table entries 32 tiles at a time (lane l -> tile t0+l,
     // one coalesced load, the next group's load in flight while this group is issued);
@@ -239,9 +235,9 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
 
   // ================= consumers =================
   const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
-  int it = 0;
+  const int grp = warp >> 2, wq4 = warp & 3;  // tile group, warp within the group
   for (int pass = 0; pass < n_pass; ++pass) {
-    const int qbase = KEYSPLIT ? 0 : pass * 64 + warp * 16;  // first q row of this warp
+    const int qbase = KEYSPLIT ? 0 : pass * 64 + wq4 * 16;  // first q row of this warp
     // ---- Q A-fragments (16 rows x D) straight from global ----
     uint32_t qa[D / 16][4];
     {
@@ -266,11 +262,12 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
     for (int n = 0; n < NT_D; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
 
-    constexpr int KW = KEYSPLIT ? TN / kConsumers : TN;  // keys per warp per tile
-    constexpr int NT_K = KW / 8;                          // n-tiles over keys
-    const int kofs = KEYSPLIT ? warp * KW : 0;
+    constexpr int KW = KEYSPLIT ? TN / 4 : TN;  // keys per warp per tile
+    constexpr int NT_K = KW / 8;                 // n-tiles over keys
+    const int kofs = KEYSPLIT ? wq4 * KW : 0;
 
-    for (int t = 0; t < ntiles; ++t, ++it) {
+    for (int t = grp; t < ntiles; t += NG) {
+      const int it = pass * ntiles + t;  // the producer's running tile index
       const int st = it % STAGES;
       mbar_wait(&full[st], (it / STAGES) & 1);
       const uint32_t kbase = smem_u32(smem + st * SM::kStage);
@@ -282,7 +279,7 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
         const int valid = (int)((r1 - r0) % TN);
         unsigned char* vb = smem + st * SM::kStage + SM::kTile;
         for (int e = lane; e < 16 * (D / 8); e += 32) {
-          const int rr = warp * 16 + e / (D / 8), chunk = e % (D / 8);
+          const int rr = wq4 * 16 + e / (D / 8), chunk = e % (D / 8);
           if (rr >= valid)
             *reinterpret_cast<uint4*>(vb + (chunk >> 3) * SM::kSlab + rr * 128 +
                                       (((chunk ^ rr) & 7) << 4)) = make_uint4(0, 0, 0, 0);
@@ -290,7 +287,7 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
         if (KEYSPLIT)
           __syncwarp();
         else
-          named_barrier_sync(1, kConsumers * 32);
+          named_barrier_sync(1, NC * 32);
       }
       // ---- S = Q K^T  (16 x KW) ----
       float sc[NT_K][4];
@@ -347,18 +344,12 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
       for (int n = 0; n < NT_K; ++n) {
         const float p0 = ex2(sc[n][0] - uA), p1 = ex2(sc[n][1] - uA);
         const float p2v = ex2(sc[n][2] - uB), p3 = ex2(sc[n][3] - uB);
+        sA += p0 + p1;
+        sB += p2v + p3;
         pa[n][0] = pack_bf16x2(p0, p1);
         pa[n][1] = pack_bf16x2(p2v, p3);
-        if (PLO) {
-          sA += p0 + p1;
-          sB += p2v + p3;
-          pl[n][0] = pack_bf16x2(p0 - bf16lo(pa[n][0]), p1 - bf16hi(pa[n][0]));
-          pl[n][1] = pack_bf16x2(p2v - bf16lo(pa[n][1]), p3 - bf16hi(pa[n][1]));
-        } else {
-          // bf16 P only: the row sum takes the same rounded weights as the P.V product
-          sA += bf16lo(pa[n][0]) + bf16hi(pa[n][0]);
-          sB += bf16lo(pa[n][1]) + bf16hi(pa[n][1]);
-        }
+        pl[n][0] = pack_bf16x2(p0 - bf16lo(pa[n][0]), p1 - bf16hi(pa[n][0]));
+        pl[n][1] = pack_bf16x2(p2v - bf16lo(pa[n][1]), p3 - bf16hi(pa[n][1]));
       }
       lA = lA * aA + sA;
       lB = lB * aB + sB;
@@ -377,13 +368,7 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
 #pragma unroll
       for (int kk = 0; kk < KW / 16; ++kk) {
         const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
-        uint32_t al[4] = {0u, 0u, 0u, 0u};
-        if (PLO) {
-          al[0] = pl[2 * kk][0];
-          al[1] = pl[2 * kk][1];
-          al[2] = pl[2 * kk + 1][0];
-          al[3] = pl[2 * kk + 1][1];
-        }
+        const uint32_t al[4] = {pl[2 * kk][0], pl[2 * kk][1], pl[2 * kk + 1][0], pl[2 * kk + 1][1]};
         const int vrow = kofs + kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
 #pragma unroll
         for (int nd = 0; nd < NT_D; nd += 2) {
@@ -394,10 +379,8 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
           ldsm_x4_t(addr, b0, b1, b2, b3);
           mma16816(o[nd], a, b0, b1);
           mma16816(o[nd + 1], a, b2, b3);
-          if (PLO) {
-            mma16816(o[nd], al, b0, b1);
-            mma16816(o[nd + 1], al, b2, b3);
-          }
+          mma16816(o[nd], al, b0, b1);
+          mma16816(o[nd + 1], al, b2, b3);
         }
       }
       fence_proxy_async_smem();  // generic-proxy zeroing above vs the next TMA write
@@ -411,11 +394,11 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
     lB += __shfl_xor_sync(0xffffffffu, lB, 2);
 
     if (KEYSPLIT) {
-      // ---- merge the 4 warp partials in shared memory (stage buffers are idle now) ----
-      float* so = reinterpret_cast<float*>(smem);             // [4][16][D]
-      float* sm = so + kConsumers * 16 * D;                   // [4][16] max
-      float* sl = sm + kConsumers * 16;                       // [4][16] sum
-      named_barrier_sync(1, kConsumers * 32);
+      // ---- merge the NC warp partials in shared memory (stage buffers are idle now) ----
+      float* so = reinterpret_cast<float*>(smem);             // [NC][16][D]
+      float* sm = so + NC * 16 * D;                           // [NC][16] max
+      float* sl = sm + NC * 16;                               // [NC][16] sum
+      named_barrier_sync(1, NC * 32);
 #pragma unroll
       for (int n = 0; n < NT_D; ++n) {
         const int c = n * 8 + t4 * 2;
@@ -430,16 +413,16 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
         sl[warp * 16 + g4] = lA;
         sl[warp * 16 + g4 + 8] = lB;
       }
-      named_barrier_sync(1, kConsumers * 32);
-      for (int e = threadIdx.x; e < QR * D; e += kConsumers * 32) {
+      named_barrier_sync(1, NC * 32);
+      for (int e = threadIdx.x; e < QR * D; e += NC * 32) {
         const int rr = e / D, c = e % D;
         float m = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < kConsumers; ++w) m = fmaxf(m, sm[w * 16 + rr]);
+        for (int w = 0; w < NC; ++w) m = fmaxf(m, sm[w * 16 + rr]);
         float l = 0.f, acc = 0.f;
         if (m > -INFINITY) {
 #pragma unroll
-          for (int w = 0; w < kConsumers; ++w) {
+          for (int w = 0; w < NC; ++w) {
             const float f = ex2(sm[w * 16 + rr] - m);
             l += sl[w * 16 + rr] * f;
             acc += so[(w * 16 + rr) * D + c] * f;
@@ -470,8 +453,9 @@ __global__ void __launch_bounds__(p2::kThreads) phase2_mma_kernel(
       }
     }
   }
-  if (gridDim.x > 1 && counters != nullptr) split_fixup<D>(smem, b, kvh, lq, hq, G, out, lse, part_stride_rows, final_out,
-                                    final_lse, counters);
+  if (gridDim.x > 1 && counters != nullptr)
+    split_fixup<D, NC * 32>(smem, b, kvh, lq, hq, G, out, lse, part_stride_rows, final_out,
+                            final_lse, counters);
 }
 
 // ------------------------------------------------------------------ host
@@ -508,24 +492,23 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   // timing experiment only (tools/decode_bench.py): skip the split fix-up (result incomplete)
   static const bool no_fix = getenv("STAR_K2_EXPERIMENT_NOFIX") != nullptr;
   if (no_fix) counters = nullptr;
-  // P.V precision: bf16 hi + lo split of P (1, default) or bf16 P with matching row sums (0)
-  static const bool plo = getenv("STAR_K2_PLO") == nullptr || atoi(getenv("STAR_K2_PLO")) != 0;
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)d));
   const int64_t part_rows = (int64_t)batch * lq * hq;
+  const bool keysplit = QR <= 16;
 #define STAR_P2M(DD, KS)                                                                        \
   do {                                                                                          \
-    auto kern = plo ? phase2_mma_kernel<DD, KS, true> : phase2_mma_kernel<DD, KS, false>;       \
+    auto kern = phase2_mma_kernel<DD, KS>;                                                      \
     const int bytes = Smem<DD>::kBytes;                                                         \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \
-    kern<<<grid, kThreads, bytes, s>>>(tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, pps,  \
-                                       page_size, kv_len, own_tail, chunk, out, lse, part_rows, sl2,   \
-                                       final_out, final_lse, counters);                          \
+    kern<<<grid, Cons<KS>::kThreads, bytes, s>>>(tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, \
+                                       pps, page_size, kv_len, own_tail, chunk, out, lse, part_rows, \
+                                       sl2, final_out, final_lse, counters);                     \
   } while (0)
   if (d == 128) {
-    if (QR <= 16) STAR_P2M(128, true); else STAR_P2M(128, false);
+    if (keysplit) STAR_P2M(128, true); else STAR_P2M(128, false);
   } else if (d == 64) {
-    if (QR <= 16) STAR_P2M(64, true); else STAR_P2M(64, false);
+    if (keysplit) STAR_P2M(64, true); else STAR_P2M(64, false);
   } else {
     return fail(STAR_ENOTSUP, "phase2 bf16 path needs head_dim 64 or 128");
   }

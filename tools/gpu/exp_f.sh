@@ -1,0 +1,10 @@
+# experiment batch F: K2 with two consumer groups
+mkdir -p gpurun_out
+O=gpurun_out/exp_f.log
+{
+timeout 600 python -m pytest tests/test_kernels_gpu.py tests/test_fullsize_gpu.py tests/test_model_gpu.py -x -q -k "phase2 or merge or decode or session" 2>&1 | tail -3
+for rows in 16384 32768 131072 1048576; do timeout 120 python tools/decode_bench.py --rows $rows --splits 0 8 16 --iters 200; done
+timeout 120 python tools/decode_bench.py --rows 32768 --batch 32 --splits 0 --iters 50
+STAR_K2_EXPERIMENT_NOFIX=1 timeout 120 python tools/decode_bench.py --rows 16384 --splits 0 --iters 200
+timeout 300 python tools/k2_err.py
+} > $O 2>&1
