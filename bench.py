@@ -335,25 +335,59 @@ def run_ours(args):
                                        hout)
             launches[0] += 2 * len(blocks)
 
-        for _ in range(max(1, args.warmup // 2)):
-            e2e_step()
-        barrier()
-        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n_e2e = max(1, min(args.steps, 5))
-        x0.record(stream)
-        for _ in range(n_e2e):
-            e2e_step()
-        x1.record(stream)
-        barrier()
-        e2e_ms = max_over_ranks(x0.elapsed_time(x1) / n_e2e)
-        ok = torch.equal(plan.out, out)  # the pipelined host path computes the same result
+        def time_e2e(fn):
+            for _ in range(max(1, args.warmup // 2)):
+                fn()
+            barrier()
+            x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n_e2e = max(1, min(args.steps, 5))
+            x0.record(stream)
+            for _ in range(n_e2e):
+                fn()
+            x1.record(stream)
+            barrier()
+            return max_over_ranks(x0.elapsed_time(x1) / n_e2e)
+
+        aug_ms = time_e2e(e2e_step)
+        aug_ok = torch.equal(plan.out, out)
+        aug_h2d = int((hq_raw.numel() + hk_raw.numel() + hv.numel()) * 2)
+        del hq_raw, hk_raw, hv
+        # context layout: each distinct context row crosses PCIe once; block 0's rows are
+        # replicated into the anchor slots on the device (first-block anchors)
+        n_ctx = plan.set_context_layout(positions.cpu().numpy())
+        uniq = torch.unique(positions)
+        assert uniq.numel() == n_ctx
+
+        def ctx_host(seed_x, heads):
+            full = ops.prng_fill((L, heads, d), seed_x, 1, 1.0, torch.bfloat16, dev)
+            h = torch.empty((n_ctx, heads, d), dtype=torch.bfloat16, pin_memory=True)
+            h.copy_(full.index_select(0, uniq))
+            return h
+
+        cq, ck, cv = ctx_host(seed ^ 1, hq), ctx_host(seed ^ 2, hkv), ctx_host(seed ^ 3, hkv)
+        plan.out.zero_()
+
+        def e2e_ctx_step():
+            pipeline.encode_layer_host_context(plan, cq, ck, cv, positions, kpool, vpool, table,
+                                               hout)
+            launches[0] += 2 * len(blocks)
+
+        e2e_ms = time_e2e(e2e_ctx_step)
+        ok = torch.equal(plan.out, out) and torch.equal(hout.to(dev), out)
         e2e = {"value": L / (e2e_ms * 1e-3), "unit": "tokens/s",
-               "h2d_bytes_per_step": int((hq_raw.numel() + hk_raw.numel() + hv.numel()) * 2),
+               "h2d_bytes_per_step": int((cq.numel() + ck.numel() + cv.numel()) * 2),
                "d2h_bytes_per_step": int(hout.numel() * 2), "ms_per_step": e2e_ms,
                "matches_device_path": bool(ok),
-               "path": "pinned host Q/K/V -> per-block pipeline (H2D | star_rope + star_phase1_fwd"
-                       " + star_kv_write | D2H) -> pinned host out"}
-        del hq_raw, hk_raw, hv, hout, plan
+               "path": "pinned host Q/K/V (context layout: each context row once) -> per-block "
+                       "pipeline (H2D | anchor rows replicated on device | star_rope + "
+                       "star_phase1_fwd + star_kv_write | D2H of every encoded row) -> pinned "
+                       "host out",
+               "augmented_layout": {"value": L / (aug_ms * 1e-3), "ms_per_step": aug_ms,
+                                    "h2d_bytes_per_step": aug_h2d,
+                                    "matches_device_path": bool(aug_ok),
+                                    "path": "pinned host Q/K/V with anchor rows repeated per "
+                                            "block (the reference's augmented layout)"}}
+        del cq, ck, cv, hout, plan
 
     # ---------------- phase-2 decode latency (B=1, one layer) ----------------
     del q_raw, k_raw, q_rot, out

@@ -6,6 +6,15 @@ per anchor-augmented block (segment): host->device copy of block i+1, the fused
 prologue (RoPE + own-row KV page write) and K1 of block i, device->host copy of the output of block i-1 —
 on three CUDA streams ordered by events.  The copies then hide behind the
 tensor-core work instead of adding to it.
+
+Two host input layouts:
+  * augmented (`encode_layer_host`): q/k/v rows exactly as the augmented blocks are
+    laid out, anchor rows repeated per block (ss/blocking.py:206-236);
+  * context (`encode_layer_host_context`): each distinct context row once.  With
+    first-block anchors (content and positions, the reference default) a block's anchor
+    rows are block 0's rows bit for bit at every layer (same tokens, positions and causal
+    prefix), so they cross PCIe once and are replicated on the device; every augmented row
+    is still encoded and returned.
 """
 
 from __future__ import annotations
@@ -34,6 +43,11 @@ class LayerEncodePlan:
     out: torch.Tensor
     cache_rows: torch.Tensor  # logical cache row per augmented row, -1 for anchor rows
     streams: tuple = field(default_factory=tuple)
+    # context layout: per segment, (dev_row, ctx_row, n) host->device ranges and
+    # (dst_row, src_row, n) device->device ranges (rows already on the device)
+    ctx_rows: int = 0
+    h2d: list = field(default_factory=list)
+    d2d: list = field(default_factory=list)
 
     @classmethod
     def create(cls, seg: Sequence[int], own: Sequence[int], hq: int, hkv: int, d: int,
@@ -53,6 +67,41 @@ class LayerEncodePlan:
         streams = tuple(torch.cuda.Stream(device) for _ in range(3))
         return cls(list(seg), list(own), c0, q, k, v, torch.empty_like(q), torch.empty_like(k),
                    torch.empty_like(q), cr.to(device), streams)
+
+    def set_context_layout(self, positions) -> int:
+        """Derive the context-layout copy plan from the augmented rows' context positions
+        (first-block anchors: a row's position is its context row).  Returns the number of
+        distinct context rows, i.e. the rows of the host buffers to pass."""
+        import numpy as np
+
+        pos = np.asarray(positions, dtype=np.int64)
+        if pos.shape[0] != self.seg[-1]:
+            raise ShapeError("one position per augmented row")
+        uniq = np.unique(pos)
+        ctx = np.searchsorted(uniq, pos)
+        placed = []  # (ctx_start, dev_start, n) ranges already on the device
+        self.h2d, self.d2d = [], []
+        for i in range(len(self.seg) - 1):
+            a_i = (self.seg[i + 1] - self.seg[i]) - self.own[i]
+            parts = [(self.seg[i], a_i), (self.seg[i] + a_i, self.own[i])]
+            h, dd = [], []
+            for r0, n in parts:
+                if n == 0:
+                    continue
+                c0 = int(ctx[r0])
+                if not np.array_equal(ctx[r0:r0 + n], np.arange(c0, c0 + n)):
+                    raise ShapeError("context layout needs contiguous context rows per part")
+                src = next((d0 + (c0 - s0) for s0, d0, m in placed if s0 <= c0 and c0 + n <= s0 + m),
+                           None)
+                if src is None:
+                    h.append((r0, c0, n))
+                    placed.append((c0, r0, n))
+                else:
+                    dd.append((r0, src, n))
+            self.h2d.append(h)
+            self.d2d.append(dd)
+        self.ctx_rows = int(uniq.shape[0])
+        return self.ctx_rows
 
 
 def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch.Tensor,
@@ -77,6 +126,54 @@ def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch
             plan.q[a:b].copy_(q_host[a:b], non_blocking=True)
             plan.k[a:b].copy_(k_host[a:b], non_blocking=True)
             plan.v[a:b].copy_(v_host[a:b], non_blocking=True)
+        ev_in = torch.cuda.Event()
+        ev_in.record(s_in)
+        with torch.cuda.stream(s_comp):
+            s_comp.wait_event(ev_in)
+            ops.rope_qkv(plan.q[a:b], plan.k[a:b], plan.v[a:b], positions[a:b], theta,
+                         q_out=plan.q_rot[a:b], k_out=plan.k_rot[a:b],
+                         cache_rows=plan.cache_rows[a:b], k_pages=k_pages, v_pages=v_pages,
+                         page_table=page_table)
+            ops.phase1_fwd(plan.q_rot[a:b], plan.k_rot[a:b], plan.v[a:b], [0, b - a],
+                           out=plan.out[a:b])
+        ev_c = torch.cuda.Event()
+        ev_c.record(s_comp)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_c)
+            out_host[a:b].copy_(plan.out[a:b], non_blocking=True)
+    cur.wait_stream(s_out)
+    cur.wait_stream(s_comp)
+
+
+def encode_layer_host_context(plan: LayerEncodePlan, q_ctx: torch.Tensor, k_ctx: torch.Tensor,
+                              v_ctx: torch.Tensor, positions: torch.Tensor, k_pages: torch.Tensor,
+                              v_pages: torch.Tensor, page_table: torch.Tensor,
+                              out_host: torch.Tensor, theta: float = 10000.0) -> None:
+    """As encode_layer_host, from pinned host q/k/v in the context layout (each distinct
+    context row once, plan.set_context_layout): rows of a block cross PCIe once, anchor
+    rows are replicated from the device copy of block 0.  out_host is the full augmented
+    output (every encoded row)."""
+    if not plan.h2d:
+        raise ShapeError("call plan.set_context_layout(positions) first")
+    if q_ctx.shape[0] != plan.ctx_rows:
+        raise ShapeError(f"context buffers need {plan.ctx_rows} rows, got {q_ctx.shape[0]}")
+    s_in, s_comp, s_out = plan.streams
+    cur = torch.cuda.current_stream(plan.q.device)
+    s_in.wait_stream(cur)
+    s_comp.wait_stream(cur)
+    s_out.wait_stream(cur)
+    n = len(plan.seg) - 1
+    for i in range(n):
+        a, b = plan.seg[i], plan.seg[i + 1]
+        with torch.cuda.stream(s_in):
+            for r0, c0, m in plan.h2d[i]:
+                plan.q[r0:r0 + m].copy_(q_ctx[c0:c0 + m], non_blocking=True)
+                plan.k[r0:r0 + m].copy_(k_ctx[c0:c0 + m], non_blocking=True)
+                plan.v[r0:r0 + m].copy_(v_ctx[c0:c0 + m], non_blocking=True)
+            for r0, src, m in plan.d2d[i]:  # anchor rows: device copies of earlier rows
+                plan.q[r0:r0 + m].copy_(plan.q[src:src + m], non_blocking=True)
+                plan.k[r0:r0 + m].copy_(plan.k[src:src + m], non_blocking=True)
+                plan.v[r0:r0 + m].copy_(plan.v[src:src + m], non_blocking=True)
         ev_in = torch.cuda.Event()
         ev_in.record(s_in)
         with torch.cuda.stream(s_comp):

@@ -119,3 +119,45 @@ def test_host_prng_matches_reference(golden_dir):
     assert [p.randint_below(256) for _ in range(200)] == list(g["randint256"])
     assert S.Prng(12).sample_sorted(100, 10) == list(g["sample_sorted_100_10"])
     assert S.Prng(13).shuffle(range(20)) == list(g["shuffle_20"])
+
+
+def _augmented_positions(L, b, a, G, rank):
+    """Context row of every augmented row of `rank`'s blocks (first-block anchors)."""
+    n = -(-L // b)
+    pos, seg, own = [], [0], []
+    for i in range(n):
+        if min(i * G // n, G - 1) != rank:
+            continue
+        o = min(b, L - i * b)
+        rows = list(range(a)) + list(range(i * b, i * b + o)) if i else list(range(o))
+        pos += rows
+        seg.append(seg[-1] + len(rows))
+        own.append(o)
+    return np.array(pos), seg, own
+
+
+@pytest.mark.parametrize("G,rank", [(1, 0), (4, 0), (4, 2), (2, 1)])
+def test_context_layout_copy_plan(G, rank):
+    """pipeline.LayerEncodePlan.set_context_layout: every augmented row is filled exactly
+    once, from the context row the reference's augment() puts there (ss/blocking.py:206-236);
+    each distinct context row crosses host->device once, repeats are device copies."""
+    from paper_2411_17116_b200 import pipeline
+
+    L, b, a = 40, 8, 8
+    pos, seg, own = _augmented_positions(L, b, a, G, rank)
+    plan = pipeline.LayerEncodePlan.__new__(pipeline.LayerEncodePlan)
+    plan.seg, plan.own = seg, own
+    n_ctx = plan.set_context_layout(pos)
+    uniq = np.unique(pos)
+    assert n_ctx == len(uniq)
+    filled = np.full(len(pos), -1)
+    h2d_rows = 0
+    for h, dd in zip(plan.h2d, plan.d2d):
+        for r0, c0, m in h:
+            filled[r0:r0 + m] = uniq[c0:c0 + m]
+            h2d_rows += m
+        for r0, src, m in dd:
+            assert (filled[src:src + m] >= 0).all()  # the source rows already landed
+            filled[r0:r0 + m] = filled[src:src + m]
+    assert (filled == pos).all()
+    assert h2d_rows == n_ctx
