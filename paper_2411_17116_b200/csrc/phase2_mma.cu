@@ -200,10 +200,15 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
       tma_prefetch(&tm_k);
       tma_prefetch(&tm_v);
     }
+    // bounded by the split's chunk, not by kv_len: the first table load does not wait for
+    // the kv_len load (tiles past the sequence end are resolved but never issued)
+    const int tiles_cap = (int)(chunk / TN);
     auto page_row = [&](int t) -> int {
-      if (t >= ntiles) return 0;
+      if (t >= tiles_cap) return 0;
       const int64_t row = r0 + (int64_t)t * TN;
-      const int64_t page = table[row / page_size];
+      const int64_t pi = row / page_size;
+      if (pi >= pages_per_seq) return 0;
+      const int64_t page = table[pi];
       return (int)((page * hkv + kvh) * page_size + row % page_size);
     };
     int it = 0;
