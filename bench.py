@@ -160,6 +160,11 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
+    if os.environ.get("STAR_BENCH_HANG_DUMP"):  # diagnostics: stack dump + exit if stuck
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["STAR_BENCH_HANG_DUMP"]), exit=True)
+
     from paper_2411_17116_b200 import ops
     from paper_2411_17116_b200.numerics import Prng  # noqa: F401  (API import check)
 
@@ -266,22 +271,27 @@ def run_ours(args):
     value = L / (ms * 1e-3)
 
     # ---------------- secondary: the same step with anchor dedup ----------------
+    # (only ranks holding block 0 and later blocks run it; every rank takes the same
+    # barriers, so the collectives stay matched)
     dedup_info = None
     if dedup_rows:
         ref_out = out.clone()
         out.fill_(float("nan"))  # every row must be rewritten by the deduplicated launch
         step(q_raw, k_raw, v, out, dedup=dedup_rows)
-        barrier()
+    barrier()
+    if dedup_rows:
         same = torch.equal(out, ref_out)
         del ref_out
         dk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
-        barrier()
+    barrier()
+    if dedup_rows:
         e0.record(stream)
         for s in range(args.steps):
             step(q_raw, k_raw, v, out, dk[s], dedup=dedup_rows)
         e1.record(stream)
-        barrier()
+    barrier()
+    if dedup_rows:
         dd_ms = e0.elapsed_time(e1) / args.steps
         dd_k1 = float(np.mean([x.elapsed_time(y) for x, y in dk]))
         n_dd = len(blocks) - 1

@@ -102,6 +102,19 @@ int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int 
                     int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
                     float* lse, int64_t dedup_anchor_rows, void* stream);
 
+/* Phase 1 over a query-row range of ONE segment: causal attention of query rows
+ * [q_begin, q_end) against keys [0, q_end) of the segment whose row 0 is at q/k/v/out.
+ * Equals causal_attention(q[q_begin:q_end], k[:q_end], v[:q_end], q_offset=q_begin)
+ * (ss/attention.py:109-122, the q_offset form); out rows [q_begin, q_end) and lse
+ * columns [q_begin, q_end) of [hq, lse_stride] are written, nothing else.  The bf16
+ * tensor-core path needs q_begin % 128 == 0 (whole q tiles).  Lets a host pipeline
+ * start a block's encode before all of it has arrived and ship its first rows while
+ * the rest computes. */
+int star_phase1_fwd_range(const void* q, const void* k, const void* v, int dtype, int64_t q_begin,
+                          int64_t q_end, int hq, int hkv, int d, int64_t q_row_stride,
+                          int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
+                          float* lse, int64_t lse_stride, void* stream);
+
 /*
  * Dense masked attention, one segment: q rows [lq] at absolute offset
  * q_offset against k/v rows [lk].  mask: 0 = "full", 1 = "causal"

@@ -170,6 +170,51 @@ int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int 
                         out_dtype, out_row_stride, lse, lse_stride, s);
 }
 
+int star_phase1_fwd_range(const void* q, const void* k, const void* v, int dtype, int64_t q_begin,
+                          int64_t q_end, int hq, int hkv, int d, int64_t q_row_stride,
+                          int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
+                          float* lse, int64_t lse_stride, void* stream) {
+  int rc = check_heads(hq, hkv, d);
+  if (rc) return rc;
+  if (out_dtype != STAR_F32 && out_dtype != STAR_BF16)
+    return fail(STAR_ECONFIG, "phase1: unknown out dtype %d", out_dtype);
+  if (q_begin < 0 || q_end < q_begin)
+    return fail(STAR_ESHAPE, "phase1 range: bad query rows [%lld, %lld)", (long long)q_begin,
+                (long long)q_end);
+  if (q_end > (1ll << 30)) return fail(STAR_ENOTSUP, "phase1 range: more than 2^30 rows");
+  if (out == nullptr) return fail(STAR_ESHAPE, "phase1: out is NULL");
+  if (q_row_stride < (int64_t)hq * d || kv_row_stride < (int64_t)hkv * d ||
+      out_row_stride < (int64_t)hq * d)
+    return fail(STAR_ESHAPE, "phase1: row stride smaller than heads*d");
+  if (lse != nullptr && lse_stride < q_end) return fail(STAR_ESHAPE, "phase1: lse stride < rows");
+  if (q_end == q_begin) return STAR_OK;
+  SegTable segs;
+  segs.n = 1;
+  segs.q_row0[0] = 0;
+  segs.k_row0[0] = 0;
+  segs.lq[0] = (int32_t)q_end;
+  segs.lk[0] = (int32_t)q_end;
+  segs.q_offset[0] = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == STAR_BF16 && (d == 64 || d == 128)) {
+    // the tensor-core kernel launches whole 128-row q tiles
+    if (q_begin % 128)
+      return fail(STAR_ECONFIG, "phase1 range: q_begin %lld is not a multiple of 128",
+                  (long long)q_begin);
+    segs.tile_lo[0] = (int32_t)(q_begin / 128);
+    return phase1_tc(q, k, v, segs, hq, hkv, d, q_end, q_row_stride, kv_row_stride, out,
+                     out_dtype == STAR_F32, out_row_stride, lse, lse_stride, s);
+  }
+  // CUDA-core path: rows [q_begin, q_end) as queries at offset q_begin
+  const size_t esz = dtype == STAR_BF16 ? 2 : 4, osz = out_dtype == STAR_BF16 ? 2 : 4;
+  segs.lq[0] = (int32_t)(q_end - q_begin);
+  segs.q_offset[0] = (int32_t)q_begin;
+  return attention_simt(static_cast<const char*>(q) + q_begin * q_row_stride * esz, k, v, dtype, segs,
+                        hq, hkv, d, q_row_stride, kv_row_stride, 1,
+                        static_cast<char*>(out) + q_begin * out_row_stride * osz, out_dtype,
+                        out_row_stride, lse == nullptr ? nullptr : lse + q_begin, lse_stride, s);
+}
+
 int star_attention_dense(const void* q, const void* k, const void* v, int dtype, int64_t lq,
                          int64_t lk, int64_t q_offset, int mask, int hq, int hkv, int d,
                          int64_t q_row_stride, int64_t kv_row_stride, void* out,

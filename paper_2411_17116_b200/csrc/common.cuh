@@ -69,6 +69,9 @@ struct SegTable {
   // s >= 1 repeat segment 0's rows exactly (first-block anchors); they are not launched —
   // segment 0's CTAs write their rows to every segment instead.
   int32_t dedup_tiles = 0;
+  // first launched 128-row q tile of a segment (query-row ranges, star_phase1_fwd_range);
+  // rows below it are neither computed nor written
+  int32_t tile_lo[kMaxSegments] = {};
 };
 
 }  // namespace star

@@ -613,7 +613,7 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
   prm.segs.tile_start[0] = 0;
   for (int i = 0; i < segs.n; ++i)
     prm.segs.tile_start[i + 1] = prm.segs.tile_start[i] + (segs.lq[i] + C::BM - 1) / C::BM -
-                                 (i > 0 ? segs.dedup_tiles : 0);
+                                 std::max(segs.tile_lo[i], i > 0 ? segs.dedup_tiles : 0);
   const int tiles = prm.segs.tile_start[segs.n];
   if (tiles == 0) return STAR_OK;
   // tuning knobs (read once): STAR_K1_POLY = share of each S row (in 32-column chunks of 4)

@@ -147,6 +147,30 @@ def phase1_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_start: Seq
     return out, lse
 
 
+def phase1_fwd_range(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_begin: int, q_end: int,
+                     out: torch.Tensor, lse: torch.Tensor | None = None):
+    """K1 over query rows [q_begin, q_end) of one segment (row 0 at q/k/v[0]) against keys
+    [0, q_end): causal_attention(q[q_begin:q_end], k[:q_end], v[:q_end], q_offset=q_begin).
+    Writes out rows [q_begin, q_end) (out covers the segment) and lse [hq, >= q_end]
+    columns [q_begin, q_end) when given."""
+    _cuda(q, k, v, out, lse)
+    rq, hq, qs = _rows_view(q, "q")
+    rk, hkv, ks = _rows_view(k, "k")
+    rv, hv, vs = _rows_view(v, "v")
+    if (rk, hkv) != (rv, hv) or ks != vs:
+        raise ShapeError("k and v must share shape and row stride")
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ConfigError("q, k, v must share a dtype")
+    if q_end > min(rq, rk) or out.shape[0] < q_end:
+        raise ShapeError("query range extends past the q/k/out rows")
+    _, _, os_ = _rows_view(out, "out")
+    lse_stride = lse.stride(0) if lse is not None else 0
+    _lib.call("star_phase1_fwd_range", q.data_ptr(), k.data_ptr(), v.data_ptr(), dtype_code(q),
+              int(q_begin), int(q_end), hq, hkv, q.shape[2], qs, ks, out.data_ptr(),
+              dtype_code(out), os_, _ptr(lse), lse_stride, _stream(q.device))
+    return out
+
+
 def attention_dense(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_offset: int = 0,
                     mask: str = "causal", want_lse: bool = True):
     """Masked attention of q [lq, hq, d] vs k/v [lk, hkv, d]; mask "causal" | "full"."""

@@ -104,16 +104,31 @@ class LayerEncodePlan:
         return self.ctx_rows
 
 
-def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch.Tensor,
-                      v_host: torch.Tensor, positions: torch.Tensor, k_pages: torch.Tensor,
-                      v_pages: torch.Tensor, page_table: torch.Tensor, out_host: torch.Tensor,
-                      theta: float = 10000.0) -> None:
-    """Phase-1 encode of one layer from pinned host q/k/v (pre-RoPE) to pinned host out.
+def _cuts(m: int, first: bool, last: bool) -> list:
+    """Query-row cut points of one segment: the first segment is encoded in two causal
+    halves (its second half's H2D overlaps the first half's K1), the last in three parts
+    (the D2H of its first rows overlaps the K1 of the rest); interior segments whole."""
+    pts = {0, m}
+    if first:
+        pts.add(m // 2)
+    if last:
+        pts.update((m // 2, 3 * m // 4))
+    return sorted({min(m, (c // 128) * 128) if c not in (0, m) else c for c in pts})
 
-    positions: device int64 [rows].  Returns when every copy and kernel is queued; the
-    caller synchronises (or records an event) on the current stream, which is made to wait
-    on the pipeline.
-    """
+
+def _clip(ranges, lo: int, hi: int):
+    """(dst_row, src_row, n) ranges restricted to destination rows [lo, hi)."""
+    out = []
+    for r0, src, n in ranges:
+        a, b = max(r0, lo), min(r0 + n, hi)
+        if a < b:
+            out.append((a, src + (a - r0), b - a))
+    return out
+
+
+def _encode(plan: LayerEncodePlan, copy_in, positions, k_pages, v_pages, page_table, out_host,
+            theta):
+    """Per segment and query-row part: H2D (copy_in) | RoPE + KV write + K1 range | D2H."""
     s_in, s_comp, s_out = plan.streams
     cur = torch.cuda.current_stream(plan.q.device)
     s_in.wait_stream(cur)
@@ -122,27 +137,48 @@ def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch
     n = len(plan.seg) - 1
     for i in range(n):
         a, b = plan.seg[i], plan.seg[i + 1]
-        with torch.cuda.stream(s_in):
-            plan.q[a:b].copy_(q_host[a:b], non_blocking=True)
-            plan.k[a:b].copy_(k_host[a:b], non_blocking=True)
-            plan.v[a:b].copy_(v_host[a:b], non_blocking=True)
-        ev_in = torch.cuda.Event()
-        ev_in.record(s_in)
-        with torch.cuda.stream(s_comp):
-            s_comp.wait_event(ev_in)
-            ops.rope_qkv(plan.q[a:b], plan.k[a:b], plan.v[a:b], positions[a:b], theta,
-                         q_out=plan.q_rot[a:b], k_out=plan.k_rot[a:b],
-                         cache_rows=plan.cache_rows[a:b], k_pages=k_pages, v_pages=v_pages,
-                         page_table=page_table)
-            ops.phase1_fwd(plan.q_rot[a:b], plan.k_rot[a:b], plan.v[a:b], [0, b - a],
-                           out=plan.out[a:b])
-        ev_c = torch.cuda.Event()
-        ev_c.record(s_comp)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(ev_c)
-            out_host[a:b].copy_(plan.out[a:b], non_blocking=True)
+        cuts = _cuts(b - a, i == 0, i == n - 1)
+        for p0, p1 in zip(cuts[:-1], cuts[1:]):
+            with torch.cuda.stream(s_in):
+                copy_in(i, a + p0, a + p1)
+            ev_in = torch.cuda.Event()
+            ev_in.record(s_in)
+            with torch.cuda.stream(s_comp):
+                s_comp.wait_event(ev_in)
+                r0, r1 = a + p0, a + p1
+                ops.rope_qkv(plan.q[r0:r1], plan.k[r0:r1], plan.v[r0:r1], positions[r0:r1], theta,
+                             q_out=plan.q_rot[r0:r1], k_out=plan.k_rot[r0:r1],
+                             cache_rows=plan.cache_rows[r0:r1], k_pages=k_pages,
+                             v_pages=v_pages, page_table=page_table)
+                # causal: query rows [p0, p1) need keys [0, p1) only — already rotated
+                ops.phase1_fwd_range(plan.q_rot[a:b], plan.k_rot[a:b], plan.v[a:b], p0, p1,
+                                     out=plan.out[a:b])
+            ev_c = torch.cuda.Event()
+            ev_c.record(s_comp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_c)
+                out_host[a + p0:a + p1].copy_(plan.out[a + p0:a + p1], non_blocking=True)
     cur.wait_stream(s_out)
     cur.wait_stream(s_comp)
+
+
+def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch.Tensor,
+                      v_host: torch.Tensor, positions: torch.Tensor, k_pages: torch.Tensor,
+                      v_pages: torch.Tensor, page_table: torch.Tensor, out_host: torch.Tensor,
+                      theta: float = 10000.0) -> None:
+    """Phase-1 encode of one layer from pinned host q/k/v (pre-RoPE, augmented layout) to
+    pinned host out.
+
+    positions: device int64 [rows].  Returns when every copy and kernel is queued; the
+    caller synchronises (or records an event) on the current stream, which is made to wait
+    on the pipeline.
+    """
+    def copy_in(i, r0, r1):
+        plan.q[r0:r1].copy_(q_host[r0:r1], non_blocking=True)
+        plan.k[r0:r1].copy_(k_host[r0:r1], non_blocking=True)
+        plan.v[r0:r1].copy_(v_host[r0:r1], non_blocking=True)
+
+    _encode(plan, copy_in, positions, k_pages, v_pages, page_table, out_host, theta)
 
 
 def encode_layer_host_context(plan: LayerEncodePlan, q_ctx: torch.Tensor, k_ctx: torch.Tensor,
@@ -157,37 +193,15 @@ def encode_layer_host_context(plan: LayerEncodePlan, q_ctx: torch.Tensor, k_ctx:
         raise ShapeError("call plan.set_context_layout(positions) first")
     if q_ctx.shape[0] != plan.ctx_rows:
         raise ShapeError(f"context buffers need {plan.ctx_rows} rows, got {q_ctx.shape[0]}")
-    s_in, s_comp, s_out = plan.streams
-    cur = torch.cuda.current_stream(plan.q.device)
-    s_in.wait_stream(cur)
-    s_comp.wait_stream(cur)
-    s_out.wait_stream(cur)
-    n = len(plan.seg) - 1
-    for i in range(n):
-        a, b = plan.seg[i], plan.seg[i + 1]
-        with torch.cuda.stream(s_in):
-            for r0, c0, m in plan.h2d[i]:
-                plan.q[r0:r0 + m].copy_(q_ctx[c0:c0 + m], non_blocking=True)
-                plan.k[r0:r0 + m].copy_(k_ctx[c0:c0 + m], non_blocking=True)
-                plan.v[r0:r0 + m].copy_(v_ctx[c0:c0 + m], non_blocking=True)
-            for r0, src, m in plan.d2d[i]:  # anchor rows: device copies of earlier rows
-                plan.q[r0:r0 + m].copy_(plan.q[src:src + m], non_blocking=True)
-                plan.k[r0:r0 + m].copy_(plan.k[src:src + m], non_blocking=True)
-                plan.v[r0:r0 + m].copy_(plan.v[src:src + m], non_blocking=True)
-        ev_in = torch.cuda.Event()
-        ev_in.record(s_in)
-        with torch.cuda.stream(s_comp):
-            s_comp.wait_event(ev_in)
-            ops.rope_qkv(plan.q[a:b], plan.k[a:b], plan.v[a:b], positions[a:b], theta,
-                         q_out=plan.q_rot[a:b], k_out=plan.k_rot[a:b],
-                         cache_rows=plan.cache_rows[a:b], k_pages=k_pages, v_pages=v_pages,
-                         page_table=page_table)
-            ops.phase1_fwd(plan.q_rot[a:b], plan.k_rot[a:b], plan.v[a:b], [0, b - a],
-                           out=plan.out[a:b])
-        ev_c = torch.cuda.Event()
-        ev_c.record(s_comp)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(ev_c)
-            out_host[a:b].copy_(plan.out[a:b], non_blocking=True)
-    cur.wait_stream(s_out)
-    cur.wait_stream(s_comp)
+
+    def copy_in(i, lo, hi):
+        for r0, c0, m in _clip(plan.h2d[i], lo, hi):
+            plan.q[r0:r0 + m].copy_(q_ctx[c0:c0 + m], non_blocking=True)
+            plan.k[r0:r0 + m].copy_(k_ctx[c0:c0 + m], non_blocking=True)
+            plan.v[r0:r0 + m].copy_(v_ctx[c0:c0 + m], non_blocking=True)
+        for r0, src, m in _clip(plan.d2d[i], lo, hi):  # anchor rows: device copies
+            plan.q[r0:r0 + m].copy_(plan.q[src:src + m], non_blocking=True)
+            plan.k[r0:r0 + m].copy_(plan.k[src:src + m], non_blocking=True)
+            plan.v[r0:r0 + m].copy_(plan.v[src:src + m], non_blocking=True)
+
+    _encode(plan, copy_in, positions, k_pages, v_pages, page_table, out_host, theta)

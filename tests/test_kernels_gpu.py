@@ -295,3 +295,38 @@ def test_fused_prologue_equals_rope_plus_kv_write(ops, dtype):
     torch.cuda.synchronize()
     assert torch.equal(qo, q_ref) and torch.equal(ko, k_ref)
     assert torch.equal(kp, kp2) and torch.equal(vp, vp2)
+
+
+@pytest.mark.parametrize("d,hq,hkv,dtype", [(128, 8, 2, torch.bfloat16), (64, 4, 4, torch.bfloat16),
+                                            (64, 4, 2, torch.float32)])
+def test_phase1_query_range(ops, d, hq, hkv, dtype):
+    """star_phase1_fwd_range == causal_attention(q[b:e], k[:e], v[:e], q_offset=b)
+    (ss/attention.py:109-122): parts of a segment reassemble the whole-segment encode
+    (bit-exact on the tensor-core path) and match the oracle's q_offset form."""
+    m = 640
+    q = ops.prng_fill((m, hq, d), 31, 1, 1.0, dtype, "cuda")
+    k = ops.prng_fill((m, hkv, d), 32, 1, 1.0, dtype, "cuda")
+    v = ops.prng_fill((m, hkv, d), 33, 1, 1.0, dtype, "cuda")
+    full, full_lse = ops.phase1_fwd(q, k, v, [0, m], want_lse=True)
+    got = torch.zeros_like(full)
+    lse = torch.zeros((hq, m), dtype=torch.float32, device="cuda")
+    for b, e in ((0, 256), (256, 384), (384, m)):
+        ops.phase1_fwd_range(q, k, v, b, e, out=got, lse=lse)
+    torch.cuda.synchronize()
+    if dtype == torch.bfloat16:
+        assert torch.equal(got, full) and torch.equal(lse, full_lse)
+    G = hq // hkv
+    qn, kn, vn = (t2n(t).astype(np.float64) for t in (q, k, v))
+    for h in (0, hq - 1):
+        ro, rl = O.causal_attention_lse(qn[256:384, h], kn[:384, h // G], vn[:384, h // G],
+                                        q_offset=256)
+        g = t2n(got[256:384, h])
+        if dtype == torch.float32:
+            np.testing.assert_allclose(g, ro, rtol=1e-5, atol=1e-6)
+        else:
+            assert normwise(g, ro) <= BF16_OUT_TOL
+        np.testing.assert_allclose(t2n(lse[h, 256:384]), rl, atol=BF16_TOL)
+    if dtype == torch.bfloat16:
+        from paper_2411_17116_b200.errors import ConfigError
+        with pytest.raises(ConfigError):
+            ops.phase1_fwd_range(q, k, v, 100, 300, out=got)  # not a whole q tile
