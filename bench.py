@@ -10,8 +10,9 @@ paged cache, one kernel) and the tcgen05 causal block encode (K1) over every
 anchor-augmented block this rank owns (one launch).  `value` = context tokens encoded per second over all ranks (strong
 scaling: the 128K context is fixed, blocks are sharded by partition()).
 After the timed steps, the per-token phase-2 decode latency (K2 split-KV
-partial over the rank's paged cache + NCCL all-gather of (out, lse) + K3
-merge) is measured the same way and reported under "decode".
+partial over the rank's paged cache; at N > 1 its epilogue pushes (out, lse) into
+every rank's box over NVLink peer memory and K3x merges) is measured the same way
+and reported under "decode".
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -165,6 +166,7 @@ def run_ours(args):
 
         faulthandler.dump_traceback_later(float(os.environ["STAR_BENCH_HANG_DUMP"]), exit=True)
 
+    from paper_2411_17116_b200 import dist as D
     from paper_2411_17116_b200 import ops
     from paper_2411_17116_b200.numerics import Prng  # noqa: F401  (API import check)
 
@@ -404,72 +406,82 @@ def run_ours(args):
     torch.cuda.empty_cache()
     qd = ops.prng_fill((1, 1, hq, d), seed ^ 4, 1, 1.0, torch.bfloat16, dev)
     kv_len = torch.tensor([own_rows], dtype=torch.int32, device=dev)
-    # K2 writes (out, lse) straight into the packed wire format [hq*d | hq] of the single
-    # all-gather; K3 merges the gathered parts in place
+    # Phase-2 exchange across ranks, two transports:
+    #  * peer (the product path): K2's epilogue stores each (sequence, kv head) group's
+    #    final partial into slot `rank` of every rank's box over NVLink peer memory and
+    #    raises a flag; K3x waits for every rank's flags and merges in ascending rank order.
+    #    At N = 1 it runs as a self-loop (one box) to measure its overhead over plain K2.
+    #  * collective (for comparison, N > 1): K2 writes (out, lse) into the packed wire
+    #    format [hq*d | hq], one NCCL all-gather, K3 merges the gathered parts in place.
     packed, po, pl = ops.packed_partial(hq, d, dev)
     gathered = torch.empty(world * hq * (d + 1), dtype=torch.float32, device=dev)
     ws = ops.Phase2Workspace()
+    if world > 1:
+        ex = D.open_peer_exchange(hq, hkv, d, dev)
+    else:
+        ex = D.local_peer_exchanges(1, hq, hkv, d, dev)[0]
 
-    def decode_step():
-        o, l = ops.phase2_partial(qd, kpool, vpool, table.view(1, -1), kv_len, own_rows,
+    def k2_only():
+        return ops.phase2_partial(qd, kpool, vpool, table.view(1, -1), kv_len, own_rows,
                                   out=po.view(1, 1, hq, d), lse=pl.view(1, 1, hq), workspace=ws)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, packed)
-            return ops.merge_packed(gathered.view(world, -1), hq, d)
-        return o, l
 
-    # capture the per-token decode (K2 [+ all-gather + K3]) in a CUDA graph: a decode loop is
-    # launch-latency bound and replays a fixed graph per token
-    decode_step()  # allocate the workspace outside capture
-    barrier()
-    graph = k2_graph = None
-    n_k2 = 20
-    try:
+    def peer_step():
+        ex.push_partial(qd, kpool, vpool, table.view(1, -1), kv_len, own_rows, workspace=ws)
+        return ex.merge(1, 1, hq, hkv)
+
+    def collective_step():
+        k2_only()
+        dist.all_gather_into_tensor(gathered, packed)
+        return ops.merge_packed(gathered.view(world, -1), hq, d)
+
+    decode_step = peer_step if world > 1 else k2_only
+
+    def capture(fn, reps=1):
+        """CUDA graph of `reps` calls of fn (a decode loop replays a fixed graph per token)."""
+        fn()  # allocate workspaces outside capture
+        torch.cuda.synchronize(dev)
+        barrier()
         side = torch.cuda.Stream(dev)
         side.wait_stream(stream)
         with torch.cuda.stream(side):
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=side):
-                decode_step()
-            k2_graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(k2_graph, stream=side):
-                for _ in range(n_k2):
-                    ops.phase2_partial(qd, kpool, vpool, table.view(1, -1), kv_len, own_rows,
-                                       workspace=ws)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(reps):
+                    fn()
         stream.wait_stream(side)
-        timing = "CUDA-graph replay; kernel_us = 100 back-to-back K2 launches"
-    except Exception as exc:  # e.g. a collective backend without graph capture
-        torch.cuda.synchronize(dev)
-        graph = None
-        timing = f"eager (graph capture failed: {type(exc).__name__})"
-    replay = graph.replay if graph is not None else decode_step
+        return g
 
-    def k2_replay():
-        if k2_graph is not None:
-            k2_graph.replay()
-        else:
-            for _ in range(n_k2):
-                ops.phase2_partial(qd, kpool, vpool, table.view(1, -1), kv_len, own_rows,
-                                   workspace=ws)
-    n_dec = 200
-    for _ in range(5):
-        replay()
-    barrier()
-    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    d0.record(stream)
-    for _ in range(n_dec):
-        replay()
-    d1.record(stream)
-    barrier()
-    dec_us = max_over_ranks(d0.elapsed_time(d1) / n_dec * 1e3)
-    k2_replay()
-    barrier()
-    d0.record(stream)
-    for _ in range(5):
-        k2_replay()
-    d1.record(stream)
-    barrier()
-    k2_us = max_over_ranks(d0.elapsed_time(d1) / (5 * n_k2) * 1e3)
+    def time_replays(g, n, per=1):
+        for _ in range(3):
+            g.replay()
+        barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for _ in range(n):
+            g.replay()
+        d1.record(stream)
+        barrier()
+        return max_over_ranks(d0.elapsed_time(d1) / (n * per) * 1e3)
+
+    # every rank captures and replays the same graphs in the same order (the peer
+    # exchange pairs the ranks' k-th exchanges)
+    graph = capture(decode_step)
+    timing = "CUDA-graph replay; kernel_us = 100 back-to-back K2 launches"
+    replay = graph.replay
+    n_k2 = 20
+    k2_graph = capture(lambda: ops.phase2_partial(qd, kpool, vpool, table.view(1, -1), kv_len,
+                                                  own_rows, workspace=ws), n_k2)
+    exch_us = time_replays(capture(peer_step), 200)
+    coll_us = None
+    if world > 1:
+        try:
+            coll_us = time_replays(capture(collective_step), 200)
+        except Exception as exc:  # a backend without graph capture
+            torch.cuda.synchronize(dev)
+            coll_us = f"unmeasured ({type(exc).__name__})"
+
+    dec_us = time_replays(graph, 200)
+    k2_us = time_replays(k2_graph, 5, per=n_k2)
     kv_bytes = own_rows * hkv * d * 2 * 2
     decode = {
         "us_per_token_per_layer": dec_us, "batch": 1, "context": L,
@@ -479,7 +491,15 @@ def run_ours(args):
                      "frac": kv_bytes / (k2_us * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6532.9),
                      "bytes_per_launch": kv_bytes,
                      "note": "K2 split-KV partial + in-GPU split merge; bytes = local KV rows x 8 heads x 128 x 2 (K,V) x 2 B"},
-        "collective": "one NCCL all_gather of packed fp32 (out | lse), hq*(d+1) per rank" if world > 1 else "none (1 rank)",
+        "exchange": ("fused peer exchange: K2 epilogue stores the partial into every rank's "
+                     "box over NVLink peer memory, K3x merges on flags (no NCCL)") if world > 1
+                    else "none (1 rank: the K2 partial is the answer)",
+        "peer_exchange_us": exch_us,
+        "peer_exchange_note": ("K2 push + K3x per token" if world > 1 else
+                               "K2 push + K3x as a one-box self-loop: the fused path's overhead "
+                               "over plain K2 at N = 1"),
+        "collective_us": coll_us,
+        "collective_note": "K2 + NCCL all_gather of packed fp32 (out | lse) + K3, for comparison",
     }
 
     if rank != 0:

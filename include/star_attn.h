@@ -194,6 +194,50 @@ int star_merge_strided(const float* outs, int64_t out_part_stride, const float* 
                        int64_t lse_part_stride, int n_parts, int64_t rows, int d, void* out,
                        int out_dtype, float* lse, void* stream);
 
+/*
+ * Peer exchange of phase-2 partials (C1 fused over NVLink / NVSwitch peer memory).
+ * Replaces the gather of every host's (out, lse) to the query host and its ordered merge
+ * (_gather_merge, ss/sim.py:178-213; merge_partials, ss/attention.py:154-173).  Every rank
+ * owns one "box" of star_exchange_box_bytes(world, cap_rows, cap_groups, d) bytes of device
+ * memory, zeroed once, and maps every other rank's box with star_ipc_open_handle (all ranks
+ * on one node).  cap_rows >= batch * lq * hq and cap_groups >= batch * hkv of every call;
+ * every call passes the same (world, cap_rows, cap_groups).  One exchange (one layer of one
+ * phase-2 forward), issued by every rank in the same order:
+ *   1. every rank delivers its partial to slot `rank` of every box: star_phase2_partial_push
+ *      (the K2 epilogue stores the final partial of each (sequence, kv head) straight into
+ *      the boxes and releases a flag per group at system scope), or star_exchange_push for a
+ *      partial already in device memory (e.g. an empty cache: out = 0, lse = -inf);
+ *   2. star_exchange_merge waits for the flags of all ranks in the rank's own box
+ *      (system-scope acquire; a rank that never delivers traps the kernel after
+ *      STAR_EXCHANGE_TIMEOUT_S, default 30 s) and merges the slots in ascending rank order
+ *      into out (f32 or bf16) / lse (nullable).
+ * Exchanges are numbered on the device (a counter in the box header, advanced by step 2),
+ * so a stream-captured CUDA graph of a decode step replays correctly; consecutive
+ * exchanges alternate between two halves of the box, so a rank may run one ahead.
+ * boxes: HOST array of `world` device pointers (boxes[rank] = this rank's own box);
+ * world <= 8.  Shapes as star_phase2_partial.  The IPC calls wrap cudaIpcGetMemHandle /
+ * cudaIpcOpenMemHandle for a pointer anywhere inside an allocation (offset = its distance
+ * from the allocation base).
+ */
+#define STAR_IPC_HANDLE_BYTES 64
+int64_t star_exchange_box_bytes(int world, int64_t cap_rows, int cap_groups, int d);
+int star_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset);
+int star_ipc_open_handle(const void* handle, int64_t offset, void** dev_ptr);
+int star_ipc_close_handle(void* dev_ptr, int64_t offset);
+int star_phase2_partial_push(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
+                             const void* k_pages, const void* v_pages, int kv_dtype,
+                             int64_t num_pages, const int32_t* page_table, int pages_per_seq,
+                             int page_size, const int32_t* kv_len, int64_t max_kv_len,
+                             int own_tail, float* out, float* lse, int n_splits, void* workspace,
+                             void* const* boxes, int world, int64_t cap_rows, int cap_groups,
+                             int rank, void* stream);
+int star_exchange_push(const float* out, const float* lse, int batch, int lq, int hq, int hkv,
+                       int d, void* const* boxes, int world, int64_t cap_rows, int cap_groups,
+                       int rank, void* stream);
+int star_exchange_merge(void* box, int world, int64_t cap_rows, int cap_groups, int batch, int lq,
+                        int hq, int hkv, int d, void* out, int out_dtype, float* lse,
+                        void* stream);
+
 /* Debug/validation: C[128x128] fp32 = A[128xK] * B^T via one tcgen05 CTA.
  * mode bit 0: B given MN-major as [K x 128]; bit 1: A staged through TMEM.
  * K multiple of 64. */

@@ -50,6 +50,19 @@ SIGNATURES = {
                            c_void_p]),
     "star_merge_strided": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int, c_int64, c_int,
                                    c_void_p, c_int, c_void_p, c_void_p]),
+    "star_exchange_box_bytes": (c_int64, [c_int, c_int64, c_int, c_int]),
+    "star_ipc_get_handle": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
+    "star_ipc_open_handle": (c_int, [c_void_p, c_int64, POINTER(c_void_p)]),
+    "star_ipc_close_handle": (c_int, [c_void_p, c_int64]),
+    "star_phase2_partial_push": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
+                                         c_void_p, c_void_p, c_int, c_int64, c_void_p, c_int,
+                                         c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p,
+                                         c_int, c_void_p, c_void_p, c_int, c_int64, c_int, c_int,
+                                         c_void_p]),
+    "star_exchange_push": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
+                                   c_void_p, c_int, c_int64, c_int, c_int, c_void_p]),
+    "star_exchange_merge": (c_int, [c_void_p, c_int, c_int64, c_int, c_int, c_int, c_int, c_int,
+                                    c_int, c_void_p, c_int, c_void_p, c_void_p]),
     "star_debug_umma_gemm": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
 }
 

@@ -6,6 +6,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "exchange.cuh"
 
 namespace star {
 
@@ -69,7 +70,16 @@ int64_t phase2_workspace_bytes(int, int, int, int, int);
 int phase2_auto_splits(int, int, int64_t, int);
 int phase2_partial(const void*, int, int, int, int, int, int, const void*, const void*, int,
                    int64_t, const int32_t*, int, int, const int32_t*, int64_t, int, float*, float*,
-                   int, void*, cudaStream_t);
+                   int, void*, const PeerPush*, cudaStream_t);
+int check_exchange(const ExchangeLayout&, void* const*, int, int64_t, int);
+PeerPush make_push(const ExchangeLayout&, void* const*, int);
+int exchange_push(const float*, const float*, int, int, int, int, int, void* const*,
+                  const ExchangeLayout&, int, cudaStream_t);
+int exchange_merge(void*, const ExchangeLayout&, int, int, int, int, int, void*, int, float*,
+                   cudaStream_t);
+int ipc_get_handle(const void*, void*, int64_t*);
+int ipc_open_handle(const void*, int64_t, void**);
+int ipc_close_handle(void*, int64_t);
 int merge(const float*, const float*, int, int64_t, int, void*, int, float*, cudaStream_t);
 int merge_strided(const float*, int64_t, const float*, int64_t, int, int64_t, int, void*, int, float*,
                   cudaStream_t);
@@ -275,7 +285,56 @@ int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, i
   return phase2_partial(q, q_dtype, batch, lq, hq, hkv, d, k_pages, v_pages, kv_dtype, num_pages,
                         page_table,
                         pages_per_seq, page_size, kv_len, max_kv_len, own_tail, out, lse, n_splits,
-                        workspace, (cudaStream_t)stream);
+                        workspace, nullptr, (cudaStream_t)stream);
+}
+
+int64_t star_exchange_box_bytes(int world, int64_t cap_rows, int cap_groups, int d) {
+  if (world < 1 || world > kMaxPeers || cap_rows < 1 || cap_groups < 1 || d < 1)
+    return fail(STAR_ESHAPE, "exchange box: bad geometry");
+  return ExchangeLayout{world, cap_rows, d, cap_groups}.bytes();
+}
+
+int star_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset) {
+  return ipc_get_handle(dev_ptr, handle, offset);
+}
+
+int star_ipc_open_handle(const void* handle, int64_t offset, void** dev_ptr) {
+  return ipc_open_handle(handle, offset, dev_ptr);
+}
+
+int star_ipc_close_handle(void* dev_ptr, int64_t offset) { return ipc_close_handle(dev_ptr, offset); }
+
+int star_phase2_partial_push(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
+                             const void* k_pages, const void* v_pages, int kv_dtype,
+                             int64_t num_pages, const int32_t* page_table, int pages_per_seq,
+                             int page_size, const int32_t* kv_len, int64_t max_kv_len,
+                             int own_tail, float* out, float* lse, int n_splits, void* workspace,
+                             void* const* boxes, int world, int64_t cap_rows, int cap_groups,
+                             int rank, void* stream) {
+  int rc = check_heads(hq, hkv, d);
+  if (rc) return rc;
+  if (batch < 1 || lq < 1) return fail(STAR_ESHAPE, "phase2: bad batch/lq");
+  const ExchangeLayout L{world, cap_rows, d, cap_groups};
+  rc = check_exchange(L, boxes, rank, (int64_t)batch * lq * hq, batch * hkv);
+  if (rc) return rc;
+  const PeerPush pp = make_push(L, boxes, rank);
+  return phase2_partial(q, q_dtype, batch, lq, hq, hkv, d, k_pages, v_pages, kv_dtype, num_pages,
+                        page_table, pages_per_seq, page_size, kv_len, max_kv_len, own_tail, out,
+                        lse, n_splits, workspace, &pp, (cudaStream_t)stream);
+}
+
+int star_exchange_push(const float* out, const float* lse, int batch, int lq, int hq, int hkv,
+                       int d, void* const* boxes, int world, int64_t cap_rows, int cap_groups,
+                       int rank, void* stream) {
+  return exchange_push(out, lse, batch, lq, hq, hkv, d, boxes,
+                       ExchangeLayout{world, cap_rows, d, cap_groups}, rank, (cudaStream_t)stream);
+}
+
+int star_exchange_merge(void* box, int world, int64_t cap_rows, int cap_groups, int batch, int lq,
+                        int hq, int hkv, int d, void* out, int out_dtype, float* lse,
+                        void* stream) {
+  return exchange_merge(box, ExchangeLayout{world, cap_rows, d, cap_groups}, batch, lq, hq, hkv, d,
+                        out, out_dtype, lse, (cudaStream_t)stream);
 }
 
 int star_merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d, void* out,

@@ -11,6 +11,7 @@
 // contiguous key range ("split") of one (sequence, kv head) and serves all
 // G = hq/hkv query heads x lq query rows of that group from each K/V tile load.
 #include "common.cuh"
+#include "exchange.cuh"
 
 namespace star {
 
@@ -407,13 +408,17 @@ static int dispatch_qrb(int QR, const void* q, int batch, int lq, int hq, int hk
 int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const void* kp,
                const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
                const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
-               float* lse, float* final_out, float* final_lse, int* counters, cudaStream_t s);
+               float* lse, float* final_out, float* final_lse, int* counters, const PeerPush& pp,
+               cudaStream_t s);
+int push_partial(const float* out, const float* lse, int batch, int lq, int hq, int hkv, int d,
+                 const PeerPush& pp, cudaStream_t s);
 
 int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
                    const void* kp, const void* vp, int kv_dtype, int64_t num_pages,
                    const int32_t* table, int pps, int page_size, const int32_t* kv_len,
                    int64_t max_kv_len, int own_tail, float* out, float* lse, int n_splits,
-                   void* workspace, cudaStream_t s) {
+                   void* workspace, const PeerPush* push, cudaStream_t s) {
+  const PeerPush none{};
   if (batch < 1 || lq < 1 || hq < 1 || hkv < 1 || hq % hkv)
     return fail(STAR_ESHAPE, "phase2: bad heads/batch (batch=%d lq=%d hq=%d hkv=%d)", batch, lq,
                 hq, hkv);
@@ -459,8 +464,11 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
     // split partials are folded inside the kernel by the last CTA of each (sequence, kv
     // head); the arrival counters live after the partials in the (zero-initialised) workspace
     int* counters = n_splits > 1 ? reinterpret_cast<int*>(workspace) : nullptr;
+    // with an exchange, the final partial of each group goes from the K2 epilogue straight
+    // into every rank's box (out / lse are then only the split workspace's neighbours)
     return phase2_mma(q, batch, lq, hq, hkv, d, kp, vp, num_pages, table, pps, page_size, kv_len,
-                      own_tail, chunk, n_splits, po, pl, out, lse, counters, s);
+                      own_tail, chunk, n_splits, po, pl, out, lse, counters,
+                      push ? *push : none, s);
   }
 #define STAR_P2_D(TQ, TKV)                                                                    \
   switch (d) {                                                                                \
@@ -486,8 +494,11 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
   }
 #undef STAR_P2_D
   if (rc != STAR_OK) return rc;
-  if (n_splits > 1) return merge(po, pl, n_splits, rows, d, out, STAR_F32, lse, s);
-  return STAR_OK;
+  if (n_splits > 1) {
+    rc = merge(po, pl, n_splits, rows, d, out, STAR_F32, lse, s);
+    if (rc != STAR_OK) return rc;
+  }
+  return push ? push_partial(out, lse, batch, lq, hq, hkv, d, *push, s) : STAR_OK;
 }
 
 }  // namespace star

@@ -17,6 +17,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "exchange.cuh"
 #include "sm100.cuh"
 
 namespace star {
@@ -83,7 +84,8 @@ __device__ __forceinline__ uint32_t swz(uint32_t slab, int row, int chunk) {
 template <int D, int NT>
 __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq, int G,
                             const float* ws_out, const float* ws_lse, int64_t part_rows,
-                            float* final_out, float* final_lse, int* counters) {
+                            float* final_out, float* final_lse, int* counters,
+                            const PeerPush& pp) {
   constexpr int PS = 16;  // splits per load round
   const int tid = threadIdx.x;
   const int nsp = gridDim.x;
@@ -98,6 +100,7 @@ __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq,
   }
   named_barrier_sync(1, NT);
   if (!*flag) return;
+  const uint32_t ep = pp.L.world ? exchange_epoch(pp) : 0u;
   for (int e0 = tid; e0 < QR * D; e0 += 2 * NT) {
     int64_t orow[2];
     int c[2];
@@ -142,8 +145,10 @@ __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq,
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       if (!ok[k]) continue;
-      final_out[orow[k] * D + c[k]] = acc[k] > 0.f ? o[k] / acc[k] : 0.f;
-      if (c[k] == 0) final_lse[orow[k]] = acc[k] > 0.f ? m[k] + __logf(acc[k]) : -INFINITY;
+      put_out(pp, ep, false, final_out, orow[k] * D + c[k], acc[k] > 0.f ? o[k] / acc[k] : 0.f);
+      if (c[k] == 0)
+        put_lse(pp, ep, false, final_lse, orow[k],
+                acc[k] > 0.f ? m[k] + __logf(acc[k]) : -INFINITY);
     }
   }
   if (tid == 0) counters[b * gridDim.y + kvh] = 0;  // re-arm for the next launch
@@ -156,7 +161,8 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
     const int32_t* __restrict__ page_table, int pages_per_seq, int page_size,
     const int32_t* __restrict__ kv_len, int own_tail, int64_t chunk, float* __restrict__ out,
     float* __restrict__ lse, int64_t part_stride_rows, float scale_log2,
-    float* __restrict__ final_out, float* __restrict__ final_lse, int* __restrict__ counters) {
+    float* __restrict__ final_out, float* __restrict__ final_lse, int* __restrict__ counters,
+    const PeerPush pp) {
   using namespace p2;
   using SM = Smem<D>;
   constexpr int NC = Cons<KEYSPLIT>::NC, NG = Cons<KEYSPLIT>::NG;
@@ -168,6 +174,9 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   uint64_t* empty = full + STAGES;
 
   const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  // a programmatic dependent (K3x of the peer exchange, which only polls the words this
+  // kernel stores) may launch now and wait on SMs beside us instead of behind a kernel boundary
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int G = hq / hkv;
   const int QR = G * lq;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -239,6 +248,8 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   }
 
   // ================= consumers =================
+  // epoch of the peer exchange this CTA's final partial belongs to (one split per group)
+  const uint32_t ep = (gridDim.x == 1 && pp.L.world > 0) ? exchange_epoch(pp) : 0u;
   const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
   const int grp = warp >> 2, wq4 = warp & 3;  // tile group, warp within the group
   for (int pass = 0; pass < n_pass; ++pass) {
@@ -434,8 +445,11 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
           }
         }
         const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
-        out_part[orow * D + c] = l > 0.f ? acc / l : 0.f;
-        if (c == 0) lse_part[orow] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+        // one split: this is the final partial (pushed to every rank's box when exchanging)
+        put_out(pp, ep, gridDim.x > 1, out_part, orow * D + c, l > 0.f ? acc / l : 0.f);
+        if (c == 0)
+          put_lse(pp, ep, gridDim.x > 1, lse_part, orow,
+                  l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY);
       }
     } else {
       // ---- each warp owns its 16 rows ----
@@ -450,17 +464,18 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
 #pragma unroll
         for (int n = 0; n < NT_D; ++n) {
           const int c = n * 8 + t4 * 2;
-          *reinterpret_cast<float2*>(out_part + orow * D + c) =
-              make_float2(o[n][2 * h] * inv, o[n][2 * h + 1] * inv);
+          put_out2(pp, ep, gridDim.x > 1, out_part, orow * D + c,
+                   make_float2(o[n][2 * h] * inv, o[n][2 * h + 1] * inv));
         }
         if (t4 == 0)
-          lse_part[orow] = ls[h] > 0.f ? (ms[h] + __log2f(ls[h])) * 0.6931471805599453f : -INFINITY;
+          put_lse(pp, ep, gridDim.x > 1, lse_part, orow,
+                  ls[h] > 0.f ? (ms[h] + __log2f(ls[h])) * 0.6931471805599453f : -INFINITY);
       }
     }
   }
   if (gridDim.x > 1 && counters != nullptr)
     split_fixup<D, NC * 32>(smem, b, kvh, lq, hq, G, out, lse, part_stride_rows, final_out,
-                            final_lse, counters);
+                            final_lse, counters, pp);
 }
 
 // ------------------------------------------------------------------ host
@@ -469,7 +484,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const void* kp,
                const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
                const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
-               float* lse, float* final_out, float* final_lse, int* counters, cudaStream_t s) {
+               float* lse, float* final_out, float* final_lse, int* counters, const PeerPush& pp,
+               cudaStream_t s) {
   using namespace p2;
   auto fn = tensor_map_encoder();
   if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
@@ -508,7 +524,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \
     kern<<<grid, Cons<KS>::kThreads, bytes, s>>>(tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, \
                                        pps, page_size, kv_len, own_tail, chunk, out, lse, part_rows, \
-                                       sl2, final_out, final_lse, counters);                     \
+                                       sl2, final_out, final_lse, counters, pp);                 \
   } while (0)
   if (d == 128) {
     if (keysplit) STAR_P2M(128, true); else STAR_P2M(128, false);

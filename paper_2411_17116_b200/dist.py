@@ -2,10 +2,13 @@
 
 Phase 1 is rank-local: rank r encodes exactly the blocks partition() assigns it
 (ss/blocking.py:68) into its own paged pool; no communication.  Phase 2 per
-layer: every rank runs K2 over its pages, the fp32 (out, lse) partials are
-all-gathered (NCCL over NVLink; 16.5 KB per rank at B = l_q = 1 for Llama-8B
-shapes) and every rank folds them with K3 in ascending rank order — the
-reference's fixed host order (ss/sim.py:189-213).  All-gather rather than
+layer: every rank runs K2 over its pages and every rank ends up with every
+rank's fp32 (out, lse) partial (16.5 KB per rank at B = l_q = 1 for Llama-8B
+shapes), folded in ascending rank order — the reference's fixed host order
+(ss/sim.py:189-213).  Two transports: the fused one (PeerExchange), where K2's
+epilogue stores the partial into every rank's box over NVLink peer memory and
+K3x merges once all flags are up; and one all-gather of the packed partials +
+K3 over the process group's backend (NCCL or gloo).  All-gather rather than
 gather-to-query-host closes the reference's unmetered return path: every rank
 gets the merged attention and can compute layer l+1's queries.
 The ledger records the reference's logical transfers on the query rank.
@@ -123,6 +126,99 @@ def gather_merge(out: torch.Tensor, lse: torch.Tensor, merge_fn: Callable | None
     return merge_fn(outs, lses)
 
 
+class PeerExchange:
+    """One rank's end of the fused phase-2 exchange (C1 over NVLink peer memory).
+
+    Replaces the NCCL all-gather + K3 of gather_merge: K2's epilogue stores the rank's final
+    partial straight into slot `rank` of every rank's box and raises a flag; K3x waits for
+    all ranks' flags in the local box and merges in ascending rank order (the reference's
+    fixed host order, ss/sim.py:189-213).  Layout / protocol: csrc/exchange.cuh.
+
+    `boxes` are device addresses, one per rank (boxes[rank] is this rank's own box, the
+    others are CUDA-IPC mappings).  Every rank runs the same sequence of exchanges (push,
+    then merge); the exchanges are numbered by a counter in each box that K3x advances, so
+    they stay in step without host bookkeeping and a captured decode graph replays.
+    """
+
+    def __init__(self, rank: int, boxes: list[int], cap_rows: int, cap_groups: int, d: int,
+                 own_box: torch.Tensor, opened: list[tuple[int, int]] | None = None):
+        self.rank, self.boxes = rank, list(boxes)
+        self.world = len(boxes)
+        self.cap_rows, self.cap_groups, self.d = cap_rows, cap_groups, d
+        self.own_box = own_box
+        self._opened = opened or []
+
+    def fits(self, batch: int, lq: int, hq: int, hkv: int, d: int) -> bool:
+        return batch * lq * hq <= self.cap_rows and batch * hkv <= self.cap_groups and d == self.d
+
+    def push_partial(self, q, k_pages, v_pages, page_table, kv_len, max_kv_len,
+                     own_tail: int = 0, n_splits: int = 0, workspace=None) -> None:
+        from . import ops
+
+        ops.phase2_partial_push(q, k_pages, v_pages, page_table, kv_len, max_kv_len, self.boxes,
+                                self.cap_rows, self.cap_groups, self.rank, own_tail, n_splits,
+                                workspace)
+
+    def push(self, out, lse, batch, lq, hq, hkv) -> None:
+        from . import ops
+
+        ops.exchange_push(out, lse, batch, lq, hq, hkv, self.boxes, self.cap_rows,
+                          self.cap_groups, self.rank)
+
+    def merge(self, batch, lq, hq, hkv, out_dtype=torch.float32):
+        from . import ops
+
+        return ops.exchange_merge(self.boxes[self.rank], self.world, self.cap_rows,
+                                  self.cap_groups, batch, lq, hq, hkv, self.d,
+                                  self.own_box.device, out_dtype)
+
+    def close(self) -> None:
+        from . import ops
+
+        for ptr, off in self._opened:
+            ops.ipc_close_handle(ptr, off)
+        self._opened = []
+
+
+def _alloc_box(world, cap_rows, cap_groups, d, device) -> torch.Tensor:
+    from . import ops
+
+    n = ops.exchange_box_bytes(world, cap_rows, cap_groups, d)
+    return torch.zeros(n, dtype=torch.uint8, device=device)
+
+
+def open_peer_exchange(cap_rows: int, cap_groups: int, d: int, device, group=None) -> PeerExchange:
+    """Collective: allocate this rank's box, swap CUDA-IPC handles with every rank (one
+    all_gather_object over `group`, any backend) and map the peers' boxes."""
+    from . import ops
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = _alloc_box(world, cap_rows, cap_groups, d, device)
+    torch.cuda.synchronize(device)  # the zeroed box is visible before any peer can write it
+    handle, off = ops.ipc_get_handle(box)
+    allh = [None] * world
+    dist.all_gather_object(allh, (handle, off), group=group)
+    boxes, opened = [], []
+    for r, (h, o) in enumerate(allh):
+        if r == rank:
+            boxes.append(box.data_ptr())
+        else:
+            ptr = ops.ipc_open_handle(h, o)
+            boxes.append(ptr)
+            opened.append((ptr, o))
+    dist.barrier(group=group)  # every box mapped everywhere before the first exchange
+    return PeerExchange(rank, boxes, cap_rows, cap_groups, d, box, opened)
+
+
+def local_peer_exchanges(world: int, cap_rows: int, cap_groups: int, d: int,
+                         device) -> list[PeerExchange]:
+    """`world` ranks' boxes in ONE process (tests, and the single-GPU bench of the exchange
+    path): same kernels and layout, plain device pointers instead of IPC mappings."""
+    boxes = [_alloc_box(world, cap_rows, cap_groups, d, device) for _ in range(world)]
+    ptrs = [b.data_ptr() for b in boxes]
+    return [PeerExchange(r, ptrs, cap_rows, cap_groups, d, boxes[r]) for r in range(world)]
+
+
 def phase2_ledger_rows(q_rank: int, nonempty_ranks, layers: int, heads: int, l_q: int, d: int):
     """Ledger rows one phase-2 forward emits, in the reference's order (ss/sim.py:203-210)."""
     rows = []
@@ -148,6 +244,7 @@ class DistSession:
     next_position: int = 0
     last_logits: torch.Tensor | None = None
     generated: list = field(default_factory=list)
+    exchange: PeerExchange | None = None  # fused C1 transport; None = all-gather + K3
 
 
 def run_phase1_dist(tokens, plan: BlockPlan, spec: AnchorSpec, weights, prng: Prng | None = None,
@@ -196,22 +293,35 @@ def _phase2_forward_dist(sess: DistSession, token_ids, positions, own_tail: int,
             sess.pool.append(li, k, v, pos)
         l = q.shape[0]
         n = sess.pool.rows(li)
-        packed, o, s = ops.packed_partial(l * H, hd, q.device)
-        if n:
-            ops.phase2_partial(q.view(1, l, H, hd).to(sess.pool.dtype).contiguous(),
-                               sess.pool.k[li], sess.pool.v[li],
-                               sess.pool.page_table.view(1, -1), sess.pool.kv_len_tensor(li),
-                               n, own_tail=own_tail if rank == sess.q_rank else 0,
-                               out=o.view(1, l, H, hd), lse=s.view(1, l, H))
-        else:
-            o.zero_()
-            s.fill_(float("-inf"))
         if nonempty is None:
             flags = torch.tensor([1 if n else 0], device=q.device)
             allf = torch.empty(world, dtype=flags.dtype, device=q.device)
             dist.all_gather_into_tensor(allf, flags, group=group)
             nonempty = [r for r in range(world) if int(allf[r])]
-        att, _ = gather_merge(o, s, group=group, packed=packed)
+        qb = q.view(1, l, H, hd).to(sess.pool.dtype).contiguous()
+        tail = own_tail if rank == sess.q_rank else 0
+        ex = sess.exchange
+        if ex is not None:
+            # fused C1: K2 stores its partial into every rank's box, K3x merges (no NCCL)
+            hkv = sess.pool.k[li].shape[1]
+            if n:
+                ex.push_partial(qb, sess.pool.k[li], sess.pool.v[li],
+                                sess.pool.page_table.view(1, -1), sess.pool.kv_len_tensor(li), n,
+                                own_tail=tail)
+            else:
+                ex.push(torch.zeros(l * H, hd, device=q.device),
+                        torch.full((l * H,), float("-inf"), device=q.device), 1, l, H, hkv)
+            att, _ = ex.merge(1, l, H, hkv)
+        else:
+            packed, o, s = ops.packed_partial(l * H, hd, q.device)
+            if n:
+                ops.phase2_partial(qb, sess.pool.k[li], sess.pool.v[li],
+                                   sess.pool.page_table.view(1, -1), sess.pool.kv_len_tensor(li),
+                                   n, own_tail=tail, out=o.view(1, l, H, hd), lse=s.view(1, l, H))
+            else:
+                o.zero_()
+                s.fill_(float("-inf"))
+            att, _ = gather_merge(o, s, group=group, packed=packed)
         x = finish_layer(x, att.view(l, H, hd), lw)
     if rank == sess.q_rank:
         sess.ledger.extend(phase2_ledger_rows(sess.q_rank, nonempty, cfg.layers, H, len(pos), hd))
@@ -219,8 +329,16 @@ def _phase2_forward_dist(sess: DistSession, token_ids, positions, own_tail: int,
 
 
 def start_session_dist(weights, tokens, plan: BlockPlan, spec: AnchorSpec, prng=None,
-                       q_rank: int | None = None, group=None):
-    """Distributed start_session (ss/sim.py:284-324): phase 1 per rank, then the query."""
+                       q_rank: int | None = None, group=None, transport: str = "auto"):
+    """Distributed start_session (ss/sim.py:284-324): phase 1 per rank, then the query.
+
+    transport: "peer" = fused C1 over CUDA-IPC peer memory (PeerExchange; all ranks on one
+    node), "collective" = one all-gather of the packed partials + K3 over the process group's
+    backend, "auto" = peer when the group runs NCCL (one GPU per rank), else collective."""
+    if transport not in ("auto", "peer", "collective"):
+        raise ConfigError(f"unknown phase-2 transport {transport!r}")
+    if transport == "auto":
+        transport = "peer" if dist.get_backend(group) == "nccl" else "collective"
     world = dist.get_world_size(group)
     L = plan.context_len
     tokens = list(tokens)
@@ -230,6 +348,11 @@ def start_session_dist(weights, tokens, plan: BlockPlan, spec: AnchorSpec, prng=
     shard, pool = run_phase1_dist(tokens[:L], plan, spec, weights, prng, group)
     q_rank = world - 1 if q_rank is None else q_rank
     sess = DistSession(weights, plan, shard, pool, q_rank)
+    if transport == "peer":
+        cfg = weights.config
+        # capacity: the query encode's l_q rows x heads (decode steps use a prefix of it)
+        sess.exchange = open_peer_exchange(len(query) * cfg.heads, pool.k[0].shape[1],
+                                           cfg.head_dim, weights.embedding.device, group)
     if dist.get_rank(group) == q_rank:
         sess.ledger += [(2, q_rank, r, "query_broadcast", len(query)) for r in range(world)
                         if r != q_rank]

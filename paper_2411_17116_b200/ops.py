@@ -245,14 +245,9 @@ class Phase2Workspace:
 _default_ws: dict = {}
 
 
-def phase2_partial(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
-                   page_table: torch.Tensor, kv_len: torch.Tensor, max_kv_len: int,
-                   own_tail: int = 0, n_splits: int = 0, out: torch.Tensor | None = None,
-                   lse: torch.Tensor | None = None, workspace: Phase2Workspace | None = None):
-    """K2: partial attention of q [B, lq, hq, d] vs each sequence's paged cache.
-
-    Returns fp32 (out [B, lq, hq, d], lse [B, lq, hq]).
-    """
+def _phase2_args(q, k_pages, v_pages, page_table, kv_len, max_kv_len, own_tail, n_splits, out,
+                 lse, workspace):
+    """Validated argument tuple of star_phase2_partial[_push] (everything but the stream)."""
     _cuda(q, k_pages, v_pages, page_table, kv_len)
     if q.dim() != 4 or not q.is_contiguous():
         raise ShapeError("q must be a contiguous [batch, lq, hq, d] tensor")
@@ -281,11 +276,98 @@ def phase2_partial(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor
         lse = torch.empty((B, lq, hq), dtype=torch.float32, device=q.device)
     nbytes = lib.star_phase2_workspace_bytes(B, lq, hq, d, n_splits)
     ws = workspace or _default_ws.setdefault(q.device, Phase2Workspace())
-    _lib.call("star_phase2_partial", q.data_ptr(), dtype_code(q), B, lq, hq, hkv, d,
-              k_pages.data_ptr(), v_pages.data_ptr(), dtype_code(k_pages), k_pages.shape[0],
-              page_table.data_ptr(),
-              pps, page_size, kv_len.data_ptr(), int(max_kv_len), int(own_tail), out.data_ptr(),
-              lse.data_ptr(), int(n_splits), ws.get(nbytes, q.device), _stream(q.device))
+    args = (q.data_ptr(), dtype_code(q), B, lq, hq, hkv, d, k_pages.data_ptr(), v_pages.data_ptr(),
+            dtype_code(k_pages), k_pages.shape[0], page_table.data_ptr(), pps, page_size,
+            kv_len.data_ptr(), int(max_kv_len), int(own_tail), out.data_ptr(), lse.data_ptr(), int(n_splits),
+            ws.get(nbytes, q.device))
+    return args, out, lse
+
+
+def phase2_partial(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
+                   page_table: torch.Tensor, kv_len: torch.Tensor, max_kv_len: int,
+                   own_tail: int = 0, n_splits: int = 0, out: torch.Tensor | None = None,
+                   lse: torch.Tensor | None = None, workspace: Phase2Workspace | None = None):
+    """K2: partial attention of q [B, lq, hq, d] vs each sequence's paged cache.
+
+    Returns fp32 (out [B, lq, hq, d], lse [B, lq, hq]).
+    """
+    args, out, lse = _phase2_args(q, k_pages, v_pages, page_table, kv_len, max_kv_len, own_tail,
+                                  n_splits, out, lse, workspace)
+    _lib.call("star_phase2_partial", *args, _stream(q.device))
+    return out, lse
+
+
+# ---------------------------------------------------------------- peer exchange (fused C1)
+def exchange_box_bytes(world: int, cap_rows: int, cap_groups: int, d: int) -> int:
+    n = _lib.load().star_exchange_box_bytes(world, cap_rows, cap_groups, d)
+    _lib.check(0 if n > 0 else int(n))
+    return int(n)
+
+
+def ipc_get_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(CUDA IPC handle of t's allocation, t's byte offset inside it)."""
+    _cuda(t)
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    _lib.call("star_ipc_get_handle", t.data_ptr(), h, ctypes.byref(off))
+    return h.raw, int(off.value)
+
+
+def ipc_open_handle(handle: bytes, offset: int) -> int:
+    """Map another process's allocation; returns the device address of (base + offset)."""
+    ptr = ctypes.c_void_p(0)
+    _lib.call("star_ipc_open_handle", ctypes.create_string_buffer(bytes(handle), 64), int(offset),
+              ctypes.byref(ptr))
+    return int(ptr.value)
+
+
+def ipc_close_handle(ptr: int, offset: int) -> None:
+    _lib.call("star_ipc_close_handle", ptr, int(offset))
+
+
+def _box_array(boxes: Sequence[int]):
+    return (ctypes.c_void_p * len(boxes))(*boxes)
+
+
+def phase2_partial_push(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
+                        page_table: torch.Tensor, kv_len: torch.Tensor, max_kv_len: int,
+                        boxes: Sequence[int], cap_rows: int, cap_groups: int, rank: int,
+                        own_tail: int = 0, n_splits: int = 0,
+                        workspace: Phase2Workspace | None = None) -> None:
+    """K2 whose epilogue stores each group's final partial into slot `rank` of every box
+    (device pointers `boxes`, one per rank) and releases the group's flag for the exchange
+    in flight (epochs are counted on the device, csrc/exchange.cuh)."""
+    args, _, _ = _phase2_args(q, k_pages, v_pages, page_table, kv_len, max_kv_len, own_tail,
+                              n_splits, None, None, workspace)
+    _lib.call("star_phase2_partial_push", *args, _box_array(boxes), len(boxes), int(cap_rows),
+              int(cap_groups), int(rank), _stream(q.device))
+
+
+def exchange_push(out: torch.Tensor, lse: torch.Tensor, batch: int, lq: int, hq: int, hkv: int,
+                  boxes: Sequence[int], cap_rows: int, cap_groups: int, rank: int) -> None:
+    """Deliver a partial already in device memory (fp32 out [B*lq*hq, d], lse) to every box."""
+    _cuda(out, lse)
+    if out.dtype != torch.float32 or lse.dtype != torch.float32:
+        raise ConfigError("partials must be fp32")
+    out, lse = out.contiguous(), lse.contiguous()
+    d = out.shape[-1]
+    if out.numel() != batch * lq * hq * d or lse.numel() != batch * lq * hq:
+        raise ShapeError("partial does not match batch x lq x hq")
+    _lib.call("star_exchange_push", out.data_ptr(), lse.data_ptr(), batch, lq, hq, hkv, d,
+              _box_array(boxes), len(boxes), int(cap_rows), int(cap_groups), int(rank),
+              _stream(out.device))
+
+
+def exchange_merge(box: int, world: int, cap_rows: int, cap_groups: int, batch: int, lq: int,
+                   hq: int, hkv: int, d: int, device, out_dtype=torch.float32):
+    """K3x: wait for every rank's partial of the exchange in flight in `box`, merge them in
+    ascending rank order and advance the box's epoch.
+    Returns (out [batch*lq*hq, d], lse [batch*lq*hq])."""
+    rows = batch * lq * hq
+    out = torch.empty((rows, d), dtype=out_dtype, device=device)
+    lse = torch.empty((rows,), dtype=torch.float32, device=device)
+    _lib.call("star_exchange_merge", box, world, int(cap_rows), int(cap_groups), batch, lq, hq,
+              hkv, d, out.data_ptr(), _DT[out_dtype], lse.data_ptr(), _stream(device))
     return out, lse
 
 

@@ -72,3 +72,48 @@ def test_ops_refuse_cpu_tensors():
     x = torch.zeros(4, 1, 8)
     with pytest.raises(DeviceError, match="no CPU fallback"):
         ops.rope(x, torch.arange(4))
+
+
+def _box_bytes(world, cap_rows, cap_groups, d):
+    """Python restatement of the exchange box layout (csrc/exchange.cuh): a 256-byte header,
+    then [2 parities][world][part] 8-byte {value, epoch} words, part = rows*(d+1) rounded
+    up to even."""
+    part = (cap_rows * (d + 1) + 1) // 2 * 2
+    return 256 + 2 * world * part * 8
+
+
+@pytest.mark.parametrize("world,rows,groups,d", [(1, 32, 8, 128), (8, 32, 8, 128), (2, 7, 3, 64),
+                                                 (8, 1024, 256, 128)])
+def test_exchange_box_layout(world, rows, groups, d):
+    lib = _lib.load()
+    assert lib.star_exchange_box_bytes(world, rows, groups, d) == _box_bytes(world, rows, groups, d)
+    assert lib.star_exchange_box_bytes(9, rows, groups, d) == _lib.STAR_ESHAPE
+
+
+def test_exchange_argument_checks():
+    """Validation paths return before any device work (fake non-NULL pointers)."""
+    lib = _lib.load()
+    boxes = (ctypes.c_void_p * 2)(0x1000, 0x2000)
+    fake = ctypes.c_void_p(0x3000)
+    # the call needs more rows than the box holds
+    rc = lib.star_exchange_push(fake, fake, 1, 2, 4, 2, 64, boxes, 2, 4, 2, 0, None)
+    with pytest.raises(ShapeError, match="box holds"):
+        _lib.check(rc)
+    # rank outside the world
+    rc = lib.star_exchange_push(fake, fake, 1, 1, 4, 2, 64, boxes, 2, 4, 2, 2, None)
+    with pytest.raises(ConfigError, match="rank"):
+        _lib.check(rc)
+    # a missing peer box
+    boxes_hole = (ctypes.c_void_p * 2)(0x1000, None)
+    rc = lib.star_exchange_push(fake, fake, 1, 1, 4, 2, 64, boxes_hole, 2, 4, 2, 0, None)
+    with pytest.raises(ShapeError, match="box of rank 1"):
+        _lib.check(rc)
+    # more peers than one node
+    boxes9 = (ctypes.c_void_p * 9)(*([0x1000] * 9))
+    rc = lib.star_exchange_push(fake, fake, 1, 1, 4, 2, 64, boxes9, 9, 4, 2, 0, None)
+    assert rc == _lib.STAR_ENOTSUP
+    rc = lib.star_exchange_merge(fake, 9, 4, 2, 1, 1, 4, 2, 128, fake, 0, None, None)
+    assert rc == _lib.STAR_ENOTSUP
+    rc = lib.star_exchange_merge(fake, 2, 4, 2, 2, 1, 4, 2, 128, fake, 0, None, None)
+    with pytest.raises(ShapeError, match="box holds"):
+        _lib.check(rc)

@@ -1,7 +1,9 @@
 """Distributed session (paper_2411_17116_b200.dist) on the B200: 2 ranks share cuda:0.
 
-NCCL refuses two ranks on one device, so the transport here is gloo over CUDA
-tensors; the kernels (K1/K2/K3) are the real ones.  Checked against the
+NCCL refuses two ranks on one device, so the process group here is gloo over CUDA
+tensors; the kernels (K1/K2/K3) are the real ones.  transport="peer" runs the fused
+exchange: each process maps the other's box through CUDA IPC (two contexts on one
+device; the GPU time-slices them while K3x waits for the other rank's flags).  Checked against the
 reference's 2-host golden: identical greedy tokens and ledger, logits within
 the fp32 tolerance of test_model_gpu.
 """
@@ -29,7 +31,7 @@ def _port():
     return p
 
 
-def _worker(rank, port, name, q):
+def _worker(rank, port, name, q, transport):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -52,8 +54,12 @@ def _worker(rank, port, name, q):
         plan = S.partition(doc["sequence_len"], doc["block_size"], doc["hosts"])
         spec = S.AnchorSpec(anchor_len=doc["anchor"]["anchor_len"])
         toks = list(g["context_tokens"]) + list(g["query_tokens"])
-        logits, sess = D.start_session_dist(w, toks, plan, spec, prng=S.Prng(doc["seed"] ^ 0xA17C4B10C4ED5EED))
+        logits, sess = D.start_session_dist(w, toks, plan, spec, prng=S.Prng(doc["seed"] ^ 0xA17C4B10C4ED5EED),
+                                            transport=transport)
         gen = D.decode_dist(sess, doc["n_generate"])
+        if sess.exchange is not None:
+            dist.barrier()  # both ranks done with each other's boxes
+            sess.exchange.close()
         err = float(np.abs(logits.cpu().numpy() - g["query_logits"]).max())
         csv = None
         if rank == sess.q_rank:
@@ -70,12 +76,13 @@ def _worker(rank, port, name, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["collective", "peer"])
 @pytest.mark.parametrize("name", ["small_n2", "small_n5h2"])
-def test_dist_session_two_ranks(name):
+def test_dist_session_two_ranks(name, transport):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, port, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, port, name, q, transport)) for r in range(2)]
     for p in procs:
         p.start()
     out = dict(q.get(timeout=300) for _ in procs)
