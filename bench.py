@@ -509,6 +509,9 @@ def run_ours(args):
         return 0
 
     sweep = None if args.no_sweep else decode_sweep(dev, hq, hkv, d, peaks.get("hbm_gbs", 6532.9))
+    shares = None
+    if not args.no_sweep and world == 1:
+        shares = config_shares(dev, peak_sus)
     cpu = None
     if not args.no_cpu_baseline:
         t, rows, reps = cpu_sample(budget_s=12.0)
@@ -535,6 +538,7 @@ def run_ours(args):
                      "flops_def": "star pairs x Hq x 4 x d (anchor query rows included)"},
         "decode": decode,
         "decode_sweep": sweep,
+        "config_shares": shares,
         "anchor_dedup": dedup_info,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -587,6 +591,45 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak):
         out.append({"batch": B, "cached_tokens": S, "us_per_token_per_layer": us,
                     "gbs": nbytes / us / 1e3, "frac_of_measured_hbm": nbytes / us / 1e3 / hbm_peak})
         del kp, vp, g
+        torch.cuda.empty_cache()
+    return out
+
+
+def config_shares(dev, tensor_peak):
+    """BASELINE configs[1..3] phase 1 on the busiest GPU of an 8-GPU run: its share is one
+    anchor-augmented block (b own rows + a anchor rows), so K1 is timed on one such segment
+    at each config's heads.  FLOPs = m(m+1)/2 pairs x Hq x 4d."""
+    import torch
+
+    from paper_2411_17116_b200 import ops
+
+    out = []
+    for name, b, a, hq, hkv, L in (("cfg2 Llama-3.1-8B 128K, b=a=16K", 16384, 16384, 32, 8, 131072),
+                                   ("cfg3 Llama-3.1-8B 1M, b=a=128K", 131072, 131072, 32, 8, 1 << 20),
+                                   ("cfg4 Llama-3.1-70B 256K, b=a=32K", 32768, 32768, 64, 8, 262144)):
+        d = 128
+        m = a + b
+        q = ops.prng_fill((m, hq, d), 31, 1, 1.0, torch.bfloat16, dev)
+        k = ops.prng_fill((m, hkv, d), 32, 1, 1.0, torch.bfloat16, dev)
+        v = ops.prng_fill((m, hkv, d), 33, 1, 1.0, torch.bfloat16, dev)
+        o = torch.empty_like(q)
+        ops.phase1_fwd(q, k, v, [0, m], out=o)
+        torch.cuda.synchronize(dev)
+        reps = 2 if m > 100000 else 5
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            ops.phase1_fwd(q, k, v, [0, m], out=o)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / reps
+        flops = m * (m + 1) // 2 * hq * 4 * d
+        tf = flops / (ms * 1e-3) / 1e12
+        out.append({"config": name, "gpu_share": f"one {m}-row augmented block x {hq} q heads "
+                    f"(the last block: busiest GPU at G = 8)", "k1_ms": ms,
+                    "flops": flops, "tflops": tf, "frac_of_measured_sustained": tf / tensor_peak,
+                    "context_tokens_per_s_at_8gpu_bound": L / (ms * 1e-3)})
+        del q, k, v, o
         torch.cuda.empty_cache()
     return out
 
