@@ -407,10 +407,11 @@ def run_ours(args):
     qd = ops.prng_fill((1, 1, hq, d), seed ^ 4, 1, 1.0, torch.bfloat16, dev)
     kv_len = torch.tensor([own_rows], dtype=torch.int32, device=dev)
     # Phase-2 exchange across ranks, two transports:
-    #  * peer (the product path): K2's epilogue stores each (sequence, kv head) group's
-    #    final partial into slot `rank` of every rank's box over NVLink peer memory and
-    #    raises a flag; K3x waits for every rank's flags and merges in ascending rank order.
-    #    At N = 1 it runs as a self-loop (one box) to measure its overhead over plain K2.
+    #  * peer (the product path, star_phase2_exchange): K2's split fix-up stores each slice
+    #    of the rank's partial into every rank's box over NVLink peer memory as {value,
+    #    epoch} words, then folds every rank's words of the same slice — the whole exchange
+    #    in one kernel.  At N = 1 it runs as a self-loop (one box) to measure its overhead
+    #    over plain K2.
     #  * collective (for comparison, N > 1): K2 writes (out, lse) into the packed wire
     #    format [hq*d | hq], one NCCL all-gather, K3 merges the gathered parts in place.
     packed, po, pl = ops.packed_partial(hq, d, dev)
@@ -426,8 +427,8 @@ def run_ours(args):
                                   out=po.view(1, 1, hq, d), lse=pl.view(1, 1, hq), workspace=ws)
 
     def peer_step():
-        ex.push_partial(qd, kpool, vpool, table.view(1, -1), kv_len, own_rows, workspace=ws)
-        return ex.merge(1, 1, hq, hkv)
+        # one kernel: partial + push to every box + merge of every rank's partial
+        return ex.exchange(qd, kpool, vpool, table.view(1, -1), kv_len, own_rows, workspace=ws)
 
     def collective_step():
         k2_only()
@@ -491,13 +492,14 @@ def run_ours(args):
                      "frac": kv_bytes / (k2_us * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6532.9),
                      "bytes_per_launch": kv_bytes,
                      "note": "K2 split-KV partial + in-GPU split merge; bytes = local KV rows x 8 heads x 128 x 2 (K,V) x 2 B"},
-        "exchange": ("fused peer exchange: K2 epilogue stores the partial into every rank's "
-                     "box over NVLink peer memory, K3x merges on flags (no NCCL)") if world > 1
+        "exchange": ("fused peer exchange, one kernel per token-layer: K2 stores its partial "
+                     "into every rank's box over NVLink peer memory and merges every rank's "
+                     "partial as the words land (no NCCL)") if world > 1
                     else "none (1 rank: the K2 partial is the answer)",
         "peer_exchange_us": exch_us,
-        "peer_exchange_note": ("K2 push + K3x per token" if world > 1 else
-                               "K2 push + K3x as a one-box self-loop: the fused path's overhead "
-                               "over plain K2 at N = 1"),
+        "peer_exchange_note": ("star_phase2_exchange per token" if world > 1 else
+                               "star_phase2_exchange as a one-box self-loop: the fused path's "
+                               "overhead over plain K2 at N = 1"),
         "collective_us": coll_us,
         "collective_note": "K2 + NCCL all_gather of packed fp32 (out | lse) + K3, for comparison",
     }

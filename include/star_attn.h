@@ -231,6 +231,17 @@ int star_phase2_partial_push(const void* q, int q_dtype, int batch, int lq, int 
                              int own_tail, float* out, float* lse, int n_splits, void* workspace,
                              void* const* boxes, int world, int64_t cap_rows, int cap_groups,
                              int rank, void* stream);
+/* The whole exchange of one layer in one call: partial attention of q over this rank's
+ * cache, delivered to every box, merged over all ranks into out fp32 [batch, lq, hq, d] /
+ * lse [batch, lq, hq].  When the K2 grid is co-resident (word-mode split fix-up) ONE kernel
+ * does all of it — each CTA pushes its slice of the partial and folds the peers' words of
+ * the same slice; otherwise K2 pushes and K3x merges (two launches). */
+int star_phase2_exchange(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
+                         const void* k_pages, const void* v_pages, int kv_dtype, int64_t num_pages,
+                         const int32_t* page_table, int pages_per_seq, int page_size,
+                         const int32_t* kv_len, int64_t max_kv_len, int own_tail, float* out,
+                         float* lse, int n_splits, void* workspace, void* const* boxes, int world,
+                         int64_t cap_rows, int cap_groups, int rank, void* stream);
 int star_exchange_push(const float* out, const float* lse, int batch, int lq, int hq, int hkv,
                        int d, void* const* boxes, int world, int64_t cap_rows, int cap_groups,
                        int rank, void* stream);

@@ -59,6 +59,11 @@ SIGNATURES = {
                                          c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p,
                                          c_int, c_void_p, c_void_p, c_int, c_int64, c_int, c_int,
                                          c_void_p]),
+    "star_phase2_exchange": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
+                                     c_void_p, c_void_p, c_int, c_int64, c_void_p, c_int, c_int,
+                                     c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int,
+                                     c_void_p, c_void_p, c_int, c_int64, c_int, c_int,
+                                     c_void_p]),
     "star_exchange_push": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
                                    c_void_p, c_int, c_int64, c_int, c_int, c_void_p]),
     "star_exchange_merge": (c_int, [c_void_p, c_int, c_int64, c_int, c_int, c_int, c_int, c_int,

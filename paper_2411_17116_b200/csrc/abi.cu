@@ -70,7 +70,7 @@ int64_t phase2_workspace_bytes(int, int, int, int, int);
 int phase2_auto_splits(int, int, int64_t, int);
 int phase2_partial(const void*, int, int, int, int, int, int, const void*, const void*, int,
                    int64_t, const int32_t*, int, int, const int32_t*, int64_t, int, float*, float*,
-                   int, void*, const PeerPush*, cudaStream_t);
+                   int, void*, const PeerPush*, int*, cudaStream_t);
 int check_exchange(const ExchangeLayout&, void* const*, int, int64_t, int);
 PeerPush make_push(const ExchangeLayout&, void* const*, int);
 int exchange_push(const float*, const float*, int, int, int, int, int, void* const*,
@@ -285,7 +285,7 @@ int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, i
   return phase2_partial(q, q_dtype, batch, lq, hq, hkv, d, k_pages, v_pages, kv_dtype, num_pages,
                         page_table,
                         pages_per_seq, page_size, kv_len, max_kv_len, own_tail, out, lse, n_splits,
-                        workspace, nullptr, (cudaStream_t)stream);
+                        workspace, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 int64_t star_exchange_box_bytes(int world, int64_t cap_rows, int cap_groups, int d) {
@@ -320,7 +320,33 @@ int star_phase2_partial_push(const void* q, int q_dtype, int batch, int lq, int 
   const PeerPush pp = make_push(L, boxes, rank);
   return phase2_partial(q, q_dtype, batch, lq, hq, hkv, d, k_pages, v_pages, kv_dtype, num_pages,
                         page_table, pages_per_seq, page_size, kv_len, max_kv_len, own_tail, out,
-                        lse, n_splits, workspace, &pp, (cudaStream_t)stream);
+                        lse, n_splits, workspace, &pp, nullptr, (cudaStream_t)stream);
+}
+
+int star_phase2_exchange(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
+                         const void* k_pages, const void* v_pages, int kv_dtype, int64_t num_pages,
+                         const int32_t* page_table, int pages_per_seq, int page_size,
+                         const int32_t* kv_len, int64_t max_kv_len, int own_tail, float* out,
+                         float* lse, int n_splits, void* workspace, void* const* boxes, int world,
+                         int64_t cap_rows, int cap_groups, int rank, void* stream) {
+  int rc = check_heads(hq, hkv, d);
+  if (rc) return rc;
+  if (batch < 1 || lq < 1) return fail(STAR_ESHAPE, "phase2: bad batch/lq");
+  if (out == nullptr || lse == nullptr) return fail(STAR_ESHAPE, "phase2 exchange: NULL out/lse");
+  const ExchangeLayout L{world, cap_rows, d, cap_groups};
+  rc = check_exchange(L, boxes, rank, (int64_t)batch * lq * hq, batch * hkv);
+  if (rc) return rc;
+  PeerPush pp = make_push(L, boxes, rank);
+  pp.merge = 1;
+  int merged = 0;
+  // the partial goes to the boxes; out / lse receive the merged result (from K2 itself when
+  // its grid is co-resident, else from K3x)
+  rc = phase2_partial(q, q_dtype, batch, lq, hq, hkv, d, k_pages, v_pages, kv_dtype, num_pages,
+                      page_table, pages_per_seq, page_size, kv_len, max_kv_len, own_tail, out, lse,
+                      n_splits, workspace, &pp, &merged, (cudaStream_t)stream);
+  if (rc || merged) return rc;
+  return exchange_merge(boxes[rank], L, batch, lq, hq, hkv, d, out, STAR_F32, lse,
+                        (cudaStream_t)stream);
 }
 
 int star_exchange_push(const float* out, const float* lse, int batch, int lq, int hq, int hkv,

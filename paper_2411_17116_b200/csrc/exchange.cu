@@ -23,6 +23,7 @@ PeerPush make_push(const ExchangeLayout& L, void* const* boxes, int rank) {
   PeerPush pp{};
   pp.L = L;
   pp.rank = rank;
+  pp.merge = 0;
   for (int r = 0; r < L.world; ++r) pp.box[r] = boxes[r];
   return pp;
 }

@@ -39,6 +39,8 @@
 namespace star {
 
 constexpr int kMaxPeers = 8;  // one NVSwitch node
+// K2 workspace header: 2048 int32 arrival counters, then 2048 uint32 word-mode epochs
+constexpr int kEpochOffsetWords = 2048;
 
 struct ExchangeLayout {
   int world;
@@ -62,6 +64,9 @@ struct PeerPush {
   void* box[kMaxPeers];
   ExchangeLayout L;
   int rank;
+  // 1: the producer also merges every rank's partial of its slice (the whole exchange in
+  // one kernel; only for a co-resident grid, see split_merge_words); 0: K3x merges
+  int merge;
 };
 
 __device__ __forceinline__ void st_word(uint2* p, float v, uint32_t e) {

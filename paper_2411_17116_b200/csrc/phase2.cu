@@ -342,15 +342,16 @@ int merge(const float* outs, const float* lses, int n_parts, int64_t rows, int d
 }
 
 // ------------------------------------------------------------------ host side
-constexpr int64_t kCounterBytes = 16384;  // 4096 (sequence, kv head) counters
+constexpr int64_t kCounterBytes = 16384;  // header: 2048 arrival counters | 2048 epochs
 
 int64_t phase2_workspace_bytes(int batch, int lq, int hq, int d, int n_splits) {
   if (n_splits <= 1) return 0;
   int64_t rows = (int64_t)batch * lq * hq;
-  // fixed header of int32 arrival counters (one per (sequence, kv head)), then partial
-  // outs + lses; the header sits at the same offset whatever the split count, so a reused
-  // workspace always finds its counters re-armed
-  return kCounterBytes + (int64_t)n_splits * rows * (d + 1) * 4;
+  // fixed header (per (sequence, kv head): int32 arrival counters of the atomic fix-up, then
+  // uint32 epochs of the word fix-up), then the split partials — fp32 (atomic mode) or
+  // 8-byte {value, epoch} words (word mode); the header sits at the same offset whatever
+  // the split count, so a reused workspace always finds its counters re-armed
+  return kCounterBytes + (int64_t)n_splits * rows * (d + 1) * 8;
 }
 
 int phase2_auto_splits(int batch, int hkv, int64_t max_kv_len, int page_size) {
@@ -408,8 +409,8 @@ static int dispatch_qrb(int QR, const void* q, int batch, int lq, int hq, int hk
 int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const void* kp,
                const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
                const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
-               float* lse, float* final_out, float* final_lse, int* counters, const PeerPush& pp,
-               cudaStream_t s);
+               float* lse, float* final_out, float* final_lse, int* counters, PeerPush pp,
+               int* merged, cudaStream_t s);
 int push_partial(const float* out, const float* lse, int batch, int lq, int hq, int hkv, int d,
                  const PeerPush& pp, cudaStream_t s);
 
@@ -417,8 +418,9 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
                    const void* kp, const void* vp, int kv_dtype, int64_t num_pages,
                    const int32_t* table, int pps, int page_size, const int32_t* kv_len,
                    int64_t max_kv_len, int own_tail, float* out, float* lse, int n_splits,
-                   void* workspace, const PeerPush* push, cudaStream_t s) {
+                   void* workspace, const PeerPush* push, int* merged, cudaStream_t s) {
   const PeerPush none{};
+  if (merged != nullptr) *merged = 0;
   if (batch < 1 || lq < 1 || hq < 1 || hkv < 1 || hq % hkv)
     return fail(STAR_ESHAPE, "phase2: bad heads/batch (batch=%d lq=%d hq=%d hkv=%d)", batch, lq,
                 hq, hkv);
@@ -451,8 +453,8 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
   int64_t rows = (int64_t)batch * lq * hq;
   if (n_splits > 1) {
     if (workspace == nullptr) return fail(STAR_ECONFIG, "phase2: workspace required for splits");
-    if ((int64_t)batch * hkv * 4 > kCounterBytes)
-      return fail(STAR_ENOTSUP, "phase2: batch x kv heads > %lld", (long long)(kCounterBytes / 4));
+    if ((int64_t)batch * hkv > kEpochOffsetWords)
+      return fail(STAR_ENOTSUP, "phase2: batch x kv heads > %d", kEpochOffsetWords);
     po = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + kCounterBytes);
     pl = po + (int64_t)n_splits * rows * d;
   }
@@ -468,7 +470,7 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
     // into every rank's box (out / lse are then only the split workspace's neighbours)
     return phase2_mma(q, batch, lq, hq, hkv, d, kp, vp, num_pages, table, pps, page_size, kv_len,
                       own_tail, chunk, n_splits, po, pl, out, lse, counters,
-                      push ? *push : none, s);
+                      push ? *push : none, merged, s);
   }
 #define STAR_P2_D(TQ, TKV)                                                                    \
   switch (d) {                                                                                \

@@ -16,6 +16,10 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include <array>
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "exchange.cuh"
 #include "sm100.cuh"
@@ -74,6 +78,31 @@ __device__ __forceinline__ uint32_t swz(uint32_t slab, int row, int chunk) {
 }
 
 }  // namespace p2
+
+#ifdef STAR_K1_TRACE
+// K2 timeline (tracing library only, tools/k2_trace.py): per CTA, globaltimer ns at
+// [0] entry, [1] first K/V tile landed (consumer warp 0), [2] main loop done (warp 0),
+// [3] split partial stored (thread 0), [4] fix-up: all splits' words seen, [5] exit
+// (thread 0), [6] fused exchange: every rank's words seen, [7] fused exchange: arrived.
+constexpr int kK2TrCtas = 2048;
+__device__ unsigned long long g_k2_trace[kK2TrCtas][8];
+__device__ __forceinline__ void k2_tr(int slot) {
+  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (cta < kK2TrCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k2_trace[cta][slot] = t;
+  }
+}
+#define K2_TR(cond, slot) \
+  do {                    \
+    if (cond) k2_tr(slot); \
+  } while (0)
+#else
+#define K2_TR(cond, slot) \
+  do {                    \
+  } while (0)
+#endif
 
 // Split-K fix-up: the last CTA of a (sequence, kv head) to finish folds the gridDim.x
 // split partials (still L2-resident) with the merge rule and re-arms the counter.
@@ -154,6 +183,148 @@ __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq,
   if (tid == 0) counters[b * gridDim.y + kvh] = 0;  // re-arm for the next launch
 }
 
+// The whole peer exchange inside K2 (pp.merge; word mode, so every CTA of every rank is
+// co-resident and a CTA waits only on the peers' CTAs of the same slice, never on an
+// unscheduled CTA): after pushing its slice of the group's partial to every box, the CTA
+// polls every rank's words of that slice in its own box and folds them in ascending rank
+// order with the merge rule of merge_partials (fp64 weights, as K3x), writing the merged
+// fp32 out / lse.  The last CTA of the grid to finish advances the box's epoch.
+template <int D, int NT>
+__device__ void exchange_merge_slice(int b, int kvh, int lq, int hq, int G, int lo, int hi,
+                                     uint32_t ep, float* out, float* lse, const PeerPush& pp) {
+  void* box = pp.box[pp.rank];
+  const int par = (int)(ep & 1u);
+  const int world = pp.L.world;
+  for (int e = lo + (int)threadIdx.x; e < hi; e += NT) {
+    const int rr = e / D, c = e % D;
+    const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
+    float lv[kMaxPeers], ov[kMaxPeers];
+    uint64_t t0 = 0;
+    for (;;) {
+      bool all = true;
+#pragma unroll
+      for (int r = 0; r < kMaxPeers; ++r) {
+        if (r >= world) break;
+        const uint2* sl = pp.L.slot(box, par, r);
+        const uint2 wl = ld_word(sl + pp.L.rows * pp.L.d + orow);
+        const uint2 wo = ld_word(sl + orow * D + c);
+        all &= (wl.y == ep) & (wo.y == ep);
+        lv[r] = __uint_as_float(wl.x);
+        ov[r] = __uint_as_float(wo.x);
+      }
+      if (all) break;
+      if (t0 == 0) t0 = globaltimer_ns();
+      if (globaltimer_ns() - t0 > 30000000000ull) __trap();  // a peer never delivered
+    }
+    K2_TR(e == lo, 6);
+    double mx = -INFINITY;
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)
+      if (r < world) mx = fmax(mx, (double)lv[r]);
+    double acc = 0.0;
+    float w[kMaxPeers];
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r) {
+      if (r >= world) break;
+      const double x = lv[r] == -INFINITY ? 0.0 : exp((double)lv[r] - mx);
+      w[r] = (float)x;
+      acc += x;
+    }
+    const float inv = acc > 0.0 ? (float)(1.0 / acc) : 0.f;
+    float o = 0.f;
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)
+      if (r < world) o = fmaf(w[r], ov[r], o);
+    out[orow * D + c] = o * inv;
+    if (c == 0 && lse != nullptr) lse[orow] = acc > 0.0 ? (float)(mx + log(acc)) : -INFINITY;
+  }
+  // every CTA of the grid read the box epoch before pushing; the last to arrive advances it
+  named_barrier_sync(1, NT);
+  if (threadIdx.x == 0) {
+    uint32_t* hdr = pp.L.header(box);
+    const uint32_t total = gridDim.x * gridDim.y * gridDim.z;
+    // no fence before the arrival: this CTA's read of the epoch completed long ago (its
+    // value addressed the pushes and the polls above), so the arrival cannot overtake it
+    if (atomicAdd(hdr + 1, 1u) == total - 1u) {
+      hdr[1] = 0u;
+      hdr[0] = ep;
+      __threadfence();
+    }
+    K2_TR(true, 7);
+  }
+}
+
+// Split fix-up without atomics or fences (word mode): every split CTA stores its partial as
+// {value, epoch} words (8-byte single-copy-atomic vector stores); then EVERY split CTA of the
+// (sequence, kv head) folds 1/nsp of the group's output elements, polling the words of all
+// splits until they carry the launch's epoch.  The host picks this mode only when the whole
+// grid is co-resident (one CTA per SM), so the spinning CTAs cannot starve a split that has
+// not started.  Against the arrival-counter fix-up this removes the fence + atomic + fence
+// round and spreads the one-CTA merge tail (two load rounds + fold) over the group
+// (tools/k2_trace.py: 16K rows, last split stored -> exit 3.8 us -> see DESIGN §3 K2).
+template <int D, int NT>
+__device__ void split_merge_words(int b, int kvh, int lq, int hq, int G, const uint2* w_out,
+                                  const uint2* w_lse, int64_t part_rows, uint32_t es,
+                                  float* final_out, float* final_lse, uint32_t* grp_epoch,
+                                  const PeerPush& pp) {
+  constexpr int PS = 16;  // splits per load round (16 lse + 16 out words in flight)
+  const int tid = threadIdx.x;
+  const int nsp = gridDim.x;
+  const int QR = G * lq;
+  const int total = QR * D;
+  const int per = (total + nsp - 1) / nsp;
+  const int lo = blockIdx.x * per, hi = min(total, lo + per);
+  named_barrier_sync(1, NT);  // this CTA's own words are visible to its polls
+  const uint32_t ep = (pp.L.world && lo < hi) ? exchange_epoch(pp) : 0u;
+  for (int e = lo + tid; e < hi; e += NT) {
+    const int rr = e / D, c = e % D;
+    const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
+    float m = -INFINITY, acc = 0.f, o = 0.f;
+    for (int p0 = 0; p0 < nsp; p0 += PS) {
+      float lv[PS], ov[PS];
+      uint64_t t0 = 0;
+      for (;;) {
+        bool all = true;
+#pragma unroll
+        for (int u = 0; u < PS; ++u) {
+          uint2 wl = make_uint2(__float_as_uint(-INFINITY), es), wo = make_uint2(0u, es);
+          if (p0 + u < nsp) {
+            wl = ld_word(w_lse + (p0 + u) * part_rows + orow);
+            wo = ld_word(w_out + ((p0 + u) * part_rows + orow) * D + c);
+          }
+          all &= (wl.y == es) & (wo.y == es);
+          lv[u] = __uint_as_float(wl.x);
+          ov[u] = __uint_as_float(wo.x);
+        }
+        if (all) break;
+        if (t0 == 0) t0 = globaltimer_ns();
+        if (globaltimer_ns() - t0 > 20000000000ull) __trap();  // a split never landed
+      }
+      K2_TR(e == lo && p0 == 0, 4);
+      float mn = m;
+#pragma unroll
+      for (int u = 0; u < PS; ++u) mn = fmaxf(mn, lv[u]);
+      if (mn == -INFINITY) continue;  // nothing visible yet (empty splits)
+      const float sc = __expf(m - mn);  // 0 while m is -inf
+      acc *= sc;
+      o *= sc;
+#pragma unroll
+      for (int u = 0; u < PS; ++u) {
+        const float w = lv[u] == -INFINITY ? 0.f : __expf(lv[u] - mn);
+        acc += w;
+        o = fmaf(w, ov[u], o);
+      }
+      m = mn;
+    }
+    put_out(pp, ep, false, final_out, orow * D + c, acc > 0.f ? o / acc : 0.f);
+    if (c == 0) put_lse(pp, ep, false, final_lse, orow, acc > 0.f ? m + __logf(acc) : -INFINITY);
+  }
+  // every split's words were seen, so every CTA of the group has read the epoch: advance it
+  // for the next launch (all CTAs of the group store the same value)
+  if (tid == 0) grp_epoch[b * gridDim.y + kvh] = es;
+  if (pp.merge) exchange_merge_slice<D, NT>(b, kvh, lq, hq, G, lo, hi, ep, final_out, final_lse, pp);
+}
+
 template <int D, bool KEYSPLIT>
 __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kernel(
     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -162,7 +333,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
     const int32_t* __restrict__ kv_len, int own_tail, int64_t chunk, float* __restrict__ out,
     float* __restrict__ lse, int64_t part_stride_rows, float scale_log2,
     float* __restrict__ final_out, float* __restrict__ final_lse, int* __restrict__ counters,
-    const PeerPush pp) {
+    uint32_t* __restrict__ grp_epoch, const PeerPush pp) {
   using namespace p2;
   using SM = Smem<D>;
   constexpr int NC = Cons<KEYSPLIT>::NC, NG = Cons<KEYSPLIT>::NG;
@@ -177,6 +348,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   // a programmatic dependent (K3x of the peer exchange, which only polls the words this
   // kernel stores) may launch now and wait on SMs beside us instead of behind a kernel boundary
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  K2_TR(threadIdx.x == 0, 0);
   const int G = hq / hkv;
   const int QR = G * lq;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -250,6 +422,13 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   // ================= consumers =================
   // epoch of the peer exchange this CTA's final partial belongs to (one split per group)
   const uint32_t ep = (gridDim.x == 1 && pp.L.world > 0) ? exchange_epoch(pp) : 0u;
+  // word-mode split fix-up: this split's partial goes out as {value, epoch} words
+  const bool words = grp_epoch != nullptr && gridDim.x > 1;
+  const uint32_t es = words ? __ldcg(grp_epoch + b * gridDim.y + kvh) + 1u : 0u;
+  uint2* const w_out = reinterpret_cast<uint2*>(out);
+  uint2* const w_lse = w_out + (int64_t)gridDim.x * part_stride_rows * D;
+  uint2* const wsp_out = w_out + (int64_t)split * part_stride_rows * D;
+  uint2* const wsp_lse = w_lse + (int64_t)split * part_stride_rows;
   const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
   const int grp = warp >> 2, wq4 = warp & 3;  // tile group, warp within the group
   for (int pass = 0; pass < n_pass; ++pass) {
@@ -286,6 +465,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
       const int it = pass * ntiles + t;  // the producer's running tile index
       const int st = it % STAGES;
       mbar_wait(&full[st], (it / STAGES) & 1);
+      K2_TR(it == 0 && threadIdx.x == 0, 1);
       const uint32_t kbase = smem_u32(smem + st * SM::kStage);
       const uint32_t vbase = kbase + SM::kTile;
       const int64_t row0 = r0 + (int64_t)t * TN + kofs;
@@ -403,6 +583,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
+    K2_TR(threadIdx.x == 0, 2);
     // row sums across the quad
     lA += __shfl_xor_sync(0xffffffffu, lA, 1);
     lA += __shfl_xor_sync(0xffffffffu, lA, 2);
@@ -446,10 +627,15 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
         }
         const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
         // one split: this is the final partial (pushed to every rank's box when exchanging)
-        put_out(pp, ep, gridDim.x > 1, out_part, orow * D + c, l > 0.f ? acc / l : 0.f);
-        if (c == 0)
-          put_lse(pp, ep, gridDim.x > 1, lse_part, orow,
-                  l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY);
+        const float vo = l > 0.f ? acc / l : 0.f;
+        const float vl = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+        if (words) {
+          st_word(wsp_out + orow * D + c, vo, es);
+          if (c == 0) st_word(wsp_lse + orow, vl, es);
+        } else {
+          put_out(pp, ep, gridDim.x > 1, out_part, orow * D + c, vo);
+          if (c == 0) put_lse(pp, ep, gridDim.x > 1, lse_part, orow, vl);
+        }
       }
     } else {
       // ---- each warp owns its 16 rows ----
@@ -464,18 +650,31 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
 #pragma unroll
         for (int n = 0; n < NT_D; ++n) {
           const int c = n * 8 + t4 * 2;
-          put_out2(pp, ep, gridDim.x > 1, out_part, orow * D + c,
-                   make_float2(o[n][2 * h] * inv, o[n][2 * h + 1] * inv));
+          const float2 v2 = make_float2(o[n][2 * h] * inv, o[n][2 * h + 1] * inv);
+          if (words)
+            st_word2(wsp_out + orow * D + c, v2, es);
+          else
+            put_out2(pp, ep, gridDim.x > 1, out_part, orow * D + c, v2);
         }
-        if (t4 == 0)
-          put_lse(pp, ep, gridDim.x > 1, lse_part, orow,
-                  ls[h] > 0.f ? (ms[h] + __log2f(ls[h])) * 0.6931471805599453f : -INFINITY);
+        if (t4 == 0) {
+          const float vl = ls[h] > 0.f ? (ms[h] + __log2f(ls[h])) * 0.6931471805599453f : -INFINITY;
+          if (words)
+            st_word(wsp_lse + orow, vl, es);
+          else
+            put_lse(pp, ep, gridDim.x > 1, lse_part, orow, vl);
+        }
       }
     }
   }
-  if (gridDim.x > 1 && counters != nullptr)
+  K2_TR(threadIdx.x == 0, 3);
+  if (words) {
+    split_merge_words<D, NC * 32>(b, kvh, lq, hq, G, w_out, w_lse, part_stride_rows, es,
+                                  final_out, final_lse, grp_epoch, pp);
+  } else if (gridDim.x > 1 && counters != nullptr) {
     split_fixup<D, NC * 32>(smem, b, kvh, lq, hq, G, out, lse, part_stride_rows, final_out,
                             final_lse, counters, pp);
+  }
+  K2_TR(threadIdx.x == 0, 5);
 }
 
 // ------------------------------------------------------------------ host
@@ -484,9 +683,10 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const void* kp,
                const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
                const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
-               float* lse, float* final_out, float* final_lse, int* counters, const PeerPush& pp,
-               cudaStream_t s) {
+               float* lse, float* final_out, float* final_lse, int* counters, PeerPush pp,
+               int* merged, cudaStream_t s) {
   using namespace p2;
+  if (merged != nullptr) *merged = 0;
   auto fn = tensor_map_encoder();
   if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if (page_size % TN) return fail(STAR_ECONFIG, "page_size must be a multiple of %d", TN);
@@ -513,8 +713,37 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   // timing experiment only (tools/decode_bench.py): skip the split fix-up (result incomplete)
   static const bool no_fix = getenv("STAR_K2_EXPERIMENT_NOFIX") != nullptr;
   if (no_fix) counters = nullptr;
+  // split fix-up: word mode (every split CTA polls the others' {value, epoch} words and
+  // folds a slice of the group) when the whole grid is co-resident, so no spinning CTA can
+  // starve one that has not started; else the arrival-counter fix-up.  STAR_K2_FIXUP=atomic forces the latter (measurement).
+  static const bool force_atomic = getenv("STAR_K2_FIXUP") != nullptr && getenv("STAR_K2_FIXUP")[0] == 'a';
+  uint32_t* grp_epoch = nullptr;
+  if (counters != nullptr && n_splits > 1 && !force_atomic &&
+      (int64_t)n_splits * batch * hkv <= num_sms())  // whole grid co-resident (1 CTA / SM)
+    grp_epoch = reinterpret_cast<uint32_t*>(counters) + kEpochOffsetWords;
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)d));
   const int64_t part_rows = (int64_t)batch * lq * hq;
+  // the in-kernel cross-rank merge needs the co-resident word-mode grid
+  if (pp.merge && (grp_epoch == nullptr || pp.L.world == 0)) pp.merge = 0;
+  if (merged != nullptr) *merged = pp.merge;
+  if (n_splits > 1 && counters != nullptr) {
+    // A word's slot position depends on (batch, lq, hq, hkv, d) and word-mode epochs count
+    // per (sequence, kv head): a workspace reused with another shape (or after the
+    // arrival-counter mode wrote floats there) could hold stale words whose epoch equals
+    // the new one.  Zero the header and this launch's partials whenever the workspace's
+    // shape or mode changes (stream-ordered; once per change, e.g. query encode -> decode).
+    static std::mutex mu;
+    static std::unordered_map<const void*, std::array<int64_t, 6>> last;
+    const std::array<int64_t, 6> sig = {batch, lq, hq, hkv, d, grp_epoch != nullptr};
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = last.find(counters);
+    if (it == last.end() || it->second != sig) {
+      const size_t bytes = (size_t)16384 + (size_t)n_splits * part_rows * (d + 1) * 8;
+      cudaError_t e = cudaMemsetAsync(counters, 0, bytes, s);
+      if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 workspace reset: %s", cudaGetErrorString(e));
+      last[counters] = sig;
+    }
+  }
   const bool keysplit = QR <= 16;
 #define STAR_P2M(DD, KS)                                                                        \
   do {                                                                                          \
@@ -524,7 +753,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \
     kern<<<grid, Cons<KS>::kThreads, bytes, s>>>(tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, \
                                        pps, page_size, kv_len, own_tail, chunk, out, lse, part_rows, \
-                                       sl2, final_out, final_lse, counters, pp);                 \
+                                       sl2, final_out, final_lse, counters, grp_epoch, pp);      \
   } while (0)
   if (d == 128) {
     if (keysplit) STAR_P2M(128, true); else STAR_P2M(128, false);
@@ -538,4 +767,18 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   return STAR_OK;
 }
 
+#ifdef STAR_K1_TRACE
+int debug_k2_trace(unsigned long long* host, int n) {
+  const int cap = kK2TrCtas * 8;
+  if (n > cap) n = cap;
+  return cudaMemcpyFromSymbol(host, g_k2_trace, n * sizeof(unsigned long long)) == cudaSuccess ? n : -4;
+}
+#endif
+
 }  // namespace star
+
+#ifdef STAR_K1_TRACE
+extern "C" int star_debug_k2_trace(unsigned long long* host, int n) {
+  return star::debug_k2_trace(host, n);
+}
+#endif

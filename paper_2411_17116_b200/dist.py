@@ -159,6 +159,16 @@ class PeerExchange:
                                 self.cap_rows, self.cap_groups, self.rank, own_tail, n_splits,
                                 workspace)
 
+    def exchange(self, q, k_pages, v_pages, page_table, kv_len, max_kv_len, own_tail: int = 0,
+                 n_splits: int = 0, workspace=None):
+        """Partial over the local cache + push + merge of every rank's partial (one kernel
+        when possible).  Returns fp32 (out [B, lq, hq, d], lse [B, lq, hq])."""
+        from . import ops
+
+        return ops.phase2_exchange(q, k_pages, v_pages, page_table, kv_len, max_kv_len,
+                                   self.boxes, self.cap_rows, self.cap_groups, self.rank,
+                                   own_tail, n_splits, workspace)
+
     def push(self, out, lse, batch, lq, hq, hkv) -> None:
         from . import ops
 
@@ -305,13 +315,14 @@ def _phase2_forward_dist(sess: DistSession, token_ids, positions, own_tail: int,
             # fused C1: K2 stores its partial into every rank's box, K3x merges (no NCCL)
             hkv = sess.pool.k[li].shape[1]
             if n:
-                ex.push_partial(qb, sess.pool.k[li], sess.pool.v[li],
-                                sess.pool.page_table.view(1, -1), sess.pool.kv_len_tensor(li), n,
-                                own_tail=tail)
+                att, _ = ex.exchange(qb, sess.pool.k[li], sess.pool.v[li],
+                                     sess.pool.page_table.view(1, -1),
+                                     sess.pool.kv_len_tensor(li), n, own_tail=tail)
+                att = att.view(l * H, hd)
             else:
                 ex.push(torch.zeros(l * H, hd, device=q.device),
                         torch.full((l * H,), float("-inf"), device=q.device), 1, l, H, hkv)
-            att, _ = ex.merge(1, l, H, hkv)
+                att, _ = ex.merge(1, l, H, hkv)
         else:
             packed, o, s = ops.packed_partial(l * H, hd, q.device)
             if n:

@@ -228,8 +228,9 @@ def kv_read(k_pages: torch.Tensor, v_pages: torch.Tensor, page_table: torch.Tens
 class Phase2Workspace:
     """Reusable device workspace for the split partials (sized on demand).
 
-    Zero-initialised: the bf16 kernel keeps per-(sequence, head) arrival counters at its
-    tail and leaves them re-armed (zero) after every launch."""
+    Zero-initialised.  Its header holds the bf16 kernel's per-(sequence, kv head) arrival
+    counters (re-armed to zero by every launch) and word-mode epochs (advanced by every
+    launch); the library re-zeroes it itself when a call changes the shape or fix-up mode."""
 
     def __init__(self):
         self.buf: torch.Tensor | None = None
@@ -341,6 +342,21 @@ def phase2_partial_push(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.T
                               n_splits, None, None, workspace)
     _lib.call("star_phase2_partial_push", *args, _box_array(boxes), len(boxes), int(cap_rows),
               int(cap_groups), int(rank), _stream(q.device))
+
+
+def phase2_exchange(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
+                    page_table: torch.Tensor, kv_len: torch.Tensor, max_kv_len: int,
+                    boxes: Sequence[int], cap_rows: int, cap_groups: int, rank: int,
+                    own_tail: int = 0, n_splits: int = 0,
+                    workspace: Phase2Workspace | None = None):
+    """One layer's whole phase-2 exchange: this rank's partial pushed to every box and every
+    rank's partials merged (one kernel when the K2 grid is co-resident, else K2 + K3x).
+    Returns fp32 (out [B, lq, hq, d], lse [B, lq, hq])."""
+    args, out, lse = _phase2_args(q, k_pages, v_pages, page_table, kv_len, max_kv_len, own_tail,
+                                  n_splits, None, None, workspace)
+    _lib.call("star_phase2_exchange", *args, _box_array(boxes), len(boxes), int(cap_rows),
+              int(cap_groups), int(rank), _stream(q.device))
+    return out, lse
 
 
 def exchange_push(out: torch.Tensor, lse: torch.Tensor, batch: int, lq: int, hq: int, hkv: int,

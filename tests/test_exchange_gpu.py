@@ -158,3 +158,45 @@ def test_exchange_rejects_oversized_call(mods):
     s = torch.zeros(16, device="cuda")
     with pytest.raises(ShapeError, match="box holds"):
         exs[0].push(o, s, 1, 4, 4, 2)
+
+
+@pytest.mark.parametrize("world,splits", [(1, 0), (3, 2), (2, 3)])
+def test_fused_exchange_one_kernel(mods, world, splits):
+    """star_phase2_exchange: partial + push + cross-rank merge in ONE K2 launch per rank
+    (co-resident word-mode grid).  Ranks run on separate streams of one GPU with small grids
+    (world x splits x hkv CTAs all resident), as they would on separate GPUs; bit-exact
+    against the unfused K2 + K3 merge, and against plain K2 for one rank."""
+    ops, D = mods
+    hq, hkv, d, ps = 8, 2, 128, 64
+    lens = [2000, 1500, 2600][:world]
+    caches = _rank_caches(lens, hkv, d, torch.bfloat16, ps, seed=21 + world)
+    _write(ops, caches)
+    exs = D.local_peer_exchanges(world, 4 * hq, hkv, d, "cuda")
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    g = torch.Generator().manual_seed(3)
+    for lq, tail in ((4, 4), (1, 0), (1, 0)):
+        q = torch.randn(1, lq, hq, d, generator=g).to(torch.bfloat16).cuda()
+        torch.cuda.synchronize()
+        outs = [None] * world
+        for r, (k, v, kp, vp, table) in enumerate(caches):
+            kv_len = torch.tensor([k.shape[0]], dtype=torch.int32, device="cuda")
+            with torch.cuda.stream(streams[r]):
+                outs[r] = exs[r].exchange(q, kp, vp, table.view(1, -1), kv_len, k.shape[0],
+                                          own_tail=tail if r == world - 1 else 0,
+                                          n_splits=splits, workspace=ops.Phase2Workspace())
+        torch.cuda.synchronize()
+        parts = []
+        for r, (k, v, kp, vp, table) in enumerate(caches):
+            kv_len = torch.tensor([k.shape[0]], dtype=torch.int32, device="cuda")
+            o, s = ops.phase2_partial(q, kp, vp, table.view(1, -1), kv_len, k.shape[0],
+                                      own_tail=tail if r == world - 1 else 0, n_splits=splits)
+            parts.append((o.view(lq * hq, d), s.view(lq * hq)))
+        if world == 1:
+            ref, ref_lse = parts[0]
+        else:
+            ref, ref_lse = ops.merge(torch.stack([p[0] for p in parts]),
+                                     torch.stack([p[1] for p in parts]))
+        for r in range(world):
+            o, s = outs[r]
+            assert torch.equal(o.view(lq * hq, d), ref), (lq, r)
+            assert torch.equal(s.view(lq * hq), ref_lse), (lq, r)

@@ -186,6 +186,9 @@ def test_kv_write_read_roundtrip(ops):
     (3, 3, 4, 2, 64, [400, 3], 4),
     (5, 0, 8, 8, 64, [1000, 2000], 7),
     (32, 32, 4, 4, 64, [1024 + 32], 0),
+    # 19 x 8 = 152 (sequence, kv head) groups >= the SM count: the arrival-counter split
+    # fix-up (fewer groups use the word fix-up, where split 0 polls the others' words)
+    (1, 0, 8, 8, 64, [300 + 37 * i for i in range(19)], 2),
 ])
 def test_phase2_partial_paged(ops, dtype, lq, own_tail, hq, hkv, d, lens, splits):
     rng = np.random.default_rng(lq * 31 + hq)
@@ -225,6 +228,37 @@ def test_phase2_partial_paged(ops, dtype, lq, own_tail, hq, hkv, d, lens, splits
             else:
                 assert normwise(got[b, :, h], o) <= BF16_TOL
                 np.testing.assert_allclose(got_lse[b, :, h], l, atol=BF16_TOL)
+
+
+def test_phase2_workspace_reuse_across_shapes(ops):
+    """One workspace, alternating shapes and split counts (query encode -> decode -> batch):
+    the word-mode fix-up's epochs and words must never pick up a stale word of another
+    layout (the library re-zeroes the workspace on a shape change)."""
+    g = torch.Generator().manual_seed(9)
+    hq, hkv, d, ps = 8, 2, 128, 64
+    L = 3000
+    pages = -(-L // ps)
+    kp = torch.randn(2 * pages, hkv, ps, d, generator=g).to(torch.bfloat16).cuda()
+    vp = torch.randn(2 * pages, hkv, ps, d, generator=g).to(torch.bfloat16).cuda()
+    table = torch.arange(2 * pages, dtype=torch.int32).view(2, pages).cuda()
+    ws = ops.Phase2Workspace()
+    ref = {}
+    for it in range(3):
+        for B, lq, splits in ((1, 4, 12), (1, 1, 16), (2, 1, 9), (1, 1, 5), (2, 3, 0)):
+            q = torch.randn(B, lq, hq, d, generator=torch.Generator().manual_seed(B * 10 + lq)).to(
+                torch.bfloat16).cuda()
+            kv_len = torch.full((B,), L, dtype=torch.int32).cuda()
+            out, lse = ops.phase2_partial(q, kp, vp, table[:B], kv_len, L, n_splits=splits,
+                                          workspace=ws)
+            key = (B, lq, splits)
+            if it == 0:
+                # independent check: a fresh workspace per call
+                o2, l2 = ops.phase2_partial(q, kp, vp, table[:B], kv_len, L, n_splits=splits,
+                                            workspace=ops.Phase2Workspace())
+                assert torch.equal(out, o2) and torch.equal(lse, l2), key
+                ref[key] = (out.clone(), lse.clone())
+            else:
+                assert torch.equal(out, ref[key][0]) and torch.equal(lse, ref[key][1]), (it, key)
 
 
 def test_merge_matches_reference(ops, golden_dir):

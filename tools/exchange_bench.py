@@ -5,7 +5,8 @@ Graph-replayed variants over a rank's paged cache of --rows rows (Llama-8B heads
   k2push    K2 whose epilogue pushes into the box (no merge: flags re-raised each time)
   push      exchange_push of a resident partial (no K2)
   push+k3x  exchange_push + K3x merge (one exchange)
-  k2push+k3x  the product decode step of one rank
+  k2push+k3x  K2 push + K3x (two launches)
+  exchange(fused)  star_phase2_exchange: partial + push + merge in one K2 launch
   --world W boxes in one process: rank 0's K2 pushes to W boxes (W-1 of them unused).
 """
 import argparse
@@ -67,6 +68,9 @@ def main():
         res["k2push"] = graph_us(lambda: ex.push_partial(q, kp, vp, table, kv_len, rows,
                                                          n_splits=args.splits, workspace=ws),
                                  dev, reps=10)
+        res["exchange(fused)"] = graph_us(
+            lambda: ex.exchange(q, kp, vp, table, kv_len, rows, n_splits=args.splits,
+                                workspace=ws), dev, reps=10)
         res["push"] = graph_us(lambda: ex.push(o, l, 1, 1, hq, hkv), dev, reps=10)
 
         def push_merge():
