@@ -592,17 +592,21 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
 
     if (KEYSPLIT) {
       // ---- merge the NC warp partials in shared memory (stage buffers are idle now) ----
-      float* so = reinterpret_cast<float*>(smem);             // [NC][16][D]
-      float* sm = so + NC * 16 * D;                           // [NC][16] max
+      // rows padded by 8 floats: the 8 fragment rows of a store land in distinct banks;
+      // only the G*lq valid rows of the 16 M rows are staged (4 of 16 in Llama-8B decode)
+      constexpr int SR = D + 8;
+      float* so = reinterpret_cast<float*>(smem);             // [NC][16][SR]
+      float* sm = so + NC * 16 * SR;                          // [NC][16] max
       float* sl = sm + NC * 16;                               // [NC][16] sum
       named_barrier_sync(1, NC * 32);
 #pragma unroll
       for (int n = 0; n < NT_D; ++n) {
         const int c = n * 8 + t4 * 2;
-        so[(warp * 16 + g4) * D + c] = o[n][0];
-        so[(warp * 16 + g4) * D + c + 1] = o[n][1];
-        so[(warp * 16 + g4 + 8) * D + c] = o[n][2];
-        so[(warp * 16 + g4 + 8) * D + c + 1] = o[n][3];
+        if (g4 < QR)
+          *reinterpret_cast<float2*>(so + (warp * 16 + g4) * SR + c) = make_float2(o[n][0], o[n][1]);
+        if (g4 + 8 < QR)
+          *reinterpret_cast<float2*>(so + (warp * 16 + g4 + 8) * SR + c) =
+              make_float2(o[n][2], o[n][3]);
       }
       if (t4 == 0) {
         sm[warp * 16 + g4] = mA;
@@ -622,7 +626,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
           for (int w = 0; w < NC; ++w) {
             const float f = ex2(sm[w * 16 + rr] - m);
             l += sl[w * 16 + rr] * f;
-            acc += so[(w * 16 + rr) * D + c] * f;
+            acc += so[(w * 16 + rr) * SR + c] * f;
           }
         }
         const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;

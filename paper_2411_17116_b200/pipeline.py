@@ -104,15 +104,32 @@ class LayerEncodePlan:
         return self.ctx_rows
 
 
+# query-row cut fractions of the first and last segments (fill and drain of the pipeline);
+# STAR_E2E_CUTS="0.125,0.25,0.5/0.5,0.75,0.875" overrides them (measurement knob)
+FIRST_CUTS = (0.5,)
+LAST_CUTS = (0.5, 0.75)
+
+
+def _cut_fracs():
+    import os
+
+    env = os.environ.get("STAR_E2E_CUTS")
+    if not env:
+        return FIRST_CUTS, LAST_CUTS
+    f, l = env.split("/")
+    return (tuple(float(x) for x in f.split(",") if x), tuple(float(x) for x in l.split(",") if x))
+
+
 def _cuts(m: int, first: bool, last: bool) -> list:
-    """Query-row cut points of one segment: the first segment is encoded in two causal
-    halves (its second half's H2D overlaps the first half's K1), the last in three parts
-    (the D2H of its first rows overlaps the K1 of the rest); interior segments whole."""
+    """Query-row cut points of one segment: the first segment is encoded in causal parts (the
+    H2D of a later part overlaps the K1 of an earlier one), the last in parts whose D2H
+    overlaps the K1 of the rest; interior segments whole.  Cuts land on 128-row q tiles."""
+    fc, lc = _cut_fracs()
     pts = {0, m}
     if first:
-        pts.add(m // 2)
+        pts.update(int(m * f) for f in fc)
     if last:
-        pts.update((m // 2, 3 * m // 4))
+        pts.update(int(m * f) for f in lc)
     return sorted({min(m, (c // 128) * 128) if c not in (0, m) else c for c in pts})
 
 
