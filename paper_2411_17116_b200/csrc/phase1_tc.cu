@@ -274,7 +274,58 @@ __device__ __forceinline__ float exp_pack_regs(const uint32_t (&sv)[4][32], uint
   return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
 }
 
-template <int D, int NQ, int POLY, bool FH, bool ONEP>
+// Speculative one-pass softmax (ONEP == 2, tiles after the first): exponentiate against the
+// running max m straight away and take the row max of the raw scores in the same pass (the
+// FMNMX3 work fills issue slots of the MUFU-bound loop instead of a pass before it).  P is
+// packed into registers but NOT stored: the caller stores it unless the new max exceeds m by
+// more than the lazy-rescale threshold — the case in which the two-step kernel uses the new
+// max — and then reloads S (still intact in TMEM) and redoes the exps, so P and the row
+// sums are bit-identical to the two-step form.  Register peak as the one-pass form: each
+// chunk's S registers die as its packed P is born.
+template <bool DIAG, bool FH>
+__device__ __forceinline__ float exp_pack_regs_spec(const uint32_t (&sv)[4][32], int lim,
+                                                    float sl2, float m, float& mraw,
+                                                    uint32_t (&pk)[4][16]) {
+  float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float p[32];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float v0 = __uint_as_float(sv[c][e]), v1 = __uint_as_float(sv[c][e + 1]);
+      const float2 x = ffma2(make_float2(v0, v1), sc2, nm2);
+      p[e] = ex2v(x.x);
+      p[e + 1] = ex2v(x.y);
+      if (DIAG) {
+        if (c * 32 + e > lim) v0 = -INFINITY;
+        if (c * 32 + e + 1 > lim) v1 = -INFINITY;
+      }
+      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(v0, v1));
+    }
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float p0 = p[e], p1 = p[e + 1];
+      if (DIAG) {
+        const int col = c * 32 + e;
+        if (col > lim) p0 = 0.f;
+        if (col + 1 > lim) p1 = 0.f;
+      }
+      const uint32_t w = pack_bf16x2v(p0, p1);
+      pk[c][e >> 1] = w;
+      float2& acc = rsum[(e >> 1) & 1];
+      if (FH)
+        acc_bf16x2(acc.x, acc.y, w);
+      else
+        acc = fadd2(acc, make_float2(bf16lo(w), bf16hi(w)));
+    }
+  }
+  mraw = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+  return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
+}
+
+template <int D, int NQ, int POLY, bool FH, int ONEP>
 __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
     phase1_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                      const __grid_constant__ CUtensorMap tm_k,
@@ -435,11 +486,12 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       const bool diag = (j == qt);
       const int lim = qrow - j * C::BN;  // columns c <= lim are visible on the diagonal tile
       // ---- pass 1: row max (raw scores; the scale is applied once to the max) ----
-      float mx;
+      float mx = -INFINITY;
       uint32_t sv[4][32];
+      const bool spec = ONEP == 2 && j > 0;  // speculative pass against the running max
       if (ONEP) {
         tmem_ld_row128(s_tm, sv);
-        mx = (diag ? row_max_regs<true>(sv, lim) : row_max_regs<false>(sv, lim)) * sl2;
+        if (!spec) mx = (diag ? row_max_regs<true>(sv, lim) : row_max_regs<false>(sv, lim)) * sl2;
       } else if (diag) {
         mx = row_max<true>(s_tm, lim) * sl2;
       } else {
@@ -447,11 +499,14 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       }
       K1_TR(tr, (i * 256 + j) * 5 + 1);
       float m_use = m_run, alpha = 1.f;
-      const bool need = (j == 0) || (mx > m_run + 8.f);
-      const bool warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
-      if (need) {
-        if (j > 0) alpha = ex2(m_run - mx);
-        m_use = mx;
+      bool need = false, warp_rescale = false;
+      if (!spec) {
+        need = (j == 0) || (mx > m_run + 8.f);
+        warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
+        if (need) {
+          if (j > 0) alpha = ex2(m_run - mx);
+          m_use = mx;
+        }
       }
       // ---- pass 2: p = 2^(s*sl2 - m), row sum, bf16 P back into TMEM ----
       // Ping-pong: the two warps of one SM sub-partition (head 0 and head 1, same TMEM lane
@@ -467,7 +522,27 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       }
       K1_TR(tr, (i * 256 + j) * 5 + 2);
       float rs;
-      if (ONEP)
+      if (spec) {
+        float mraw;
+        uint32_t pk[4][16];
+        rs = diag ? exp_pack_regs_spec<true, FH>(sv, lim, sl2, m_run, mraw, pk)
+                  : exp_pack_regs_spec<false, FH>(sv, lim, sl2, m_run, mraw, pk);
+        mx = mraw * sl2;
+        need = mx > m_run + 8.f;
+        warp_rescale = __any_sync(0xffffffffu, need);
+        if (!warp_rescale) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tmem_st16(s_tm + c * 16, pk[c]);
+        } else {  // rare: S is intact in TMEM; redo against the new max as the two-step form
+          if (need) {
+            alpha = ex2(m_run - mx);
+            m_use = mx;
+          }
+          tmem_ld_row128(s_tm, sv);
+          rs = diag ? exp_pack_regs<true, 0, FH>(sv, s_tm, lim, sl2, m_use)
+                    : exp_pack_regs<false, 0, FH>(sv, s_tm, lim, sl2, m_use);
+        }
+      } else if (ONEP)
         rs = diag ? exp_pack_regs<true, POLY, FH>(sv, s_tm, lim, sl2, m_use)
                   : exp_pack_regs<false, POLY, FH>(sv, s_tm, lim, sl2, m_use);
       else
@@ -555,6 +630,7 @@ constexpr int kDefaultPoly = 0;
 constexpr int kDefaultSeq = 1;
 constexpr int kDefaultFH = 1;
 constexpr int kDefaultOnePass = 1;
+constexpr int kDefaultSpec = 0;  // speculative one-pass softmax (STAR_K1_SPEC)
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -619,7 +695,7 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
   // tuning knobs (read once): STAR_K1_POLY = share of each S row (in 32-column chunks of 4)
   // whose exp2 runs on the FMA pipe; STAR_K1_SEQ = softmax ping-pong; STAR_K1_FH = row sum
   // by f32+bf16 adds (1) or unpack + FADD2 (0)
-  static int poly = -1, seq = -1, fh = -1, onep = -1;
+  static int poly = -1, seq = -1, fh = -1, onep = -1, spec = -1;
   if (poly < 0) {
     const char* env = getenv("STAR_K1_POLY");
     poly = env ? atoi(env) : kDefaultPoly;
@@ -630,6 +706,8 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
     fh = env ? (atoi(env) != 0) : kDefaultFH;
     env = getenv("STAR_K1_ONEP");
     onep = env ? (atoi(env) != 0) : kDefaultOnePass;
+    env = getenv("STAR_K1_SPEC");
+    spec = env ? (atoi(env) != 0) : kDefaultSpec;
   }
   prm.seq = seq;
   using KernFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, P1Params);
@@ -642,7 +720,9 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
         phase1_tc_kernel<D, NQ, 2, false, true>},
        {phase1_tc_kernel<D, NQ, 0, true, true>, phase1_tc_kernel<D, NQ, 1, true, true>,
         phase1_tc_kernel<D, NQ, 2, true, true>}}};
-  const KernFn kern = table[onep][fh][poly];
+  static const KernFn spec_table[2] = {phase1_tc_kernel<D, NQ, 0, false, 2>,
+                                       phase1_tc_kernel<D, NQ, 0, true, 2>};
+  const KernFn kern = (onep && spec && poly == 0) ? spec_table[fh] : table[onep][fh][poly];
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
   dim3 grid(tiles * hkv * (hq / hkv / NQ));

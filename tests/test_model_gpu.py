@@ -135,6 +135,13 @@ def test_drop_in_attention_functions(S, golden_dir):
         S.merge_partials([])
     with pytest.raises(S.ShapeError):
         S.causal_attention(g["c2_q"], g["c2_k"], g["c2_v"], q_offset=16)
+    # streaming_causal_attention (ss/attention.py:176-210) against the reference's tile-3 fold
+    for case in ("c0", "c1", "c2", "c3"):
+        out = S.streaming_causal_attention(g[f"{case}_q"], g[f"{case}_k"], g[f"{case}_v"], 3,
+                                           q_offset=int(g[f"{case}_off"]))
+        np.testing.assert_allclose(out.cpu().numpy(), g[f"{case}_stream3"], rtol=1e-5, atol=1e-6)
+    with pytest.raises(S.ConfigError):
+        S.streaming_causal_attention(g["c1_q"], g["c1_k"], g["c1_v"], 0)
 
 
 @pytest.mark.parametrize("name", ["tiny_s4", "tiny_s7"])

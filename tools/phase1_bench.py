@@ -15,6 +15,7 @@ p.add_argument("--b", type=int, default=16384)
 p.add_argument("--hq", type=int, default=32)
 p.add_argument("--hkv", type=int, default=8)
 p.add_argument("--iters", type=int, default=5)
+p.add_argument("--save", default=None, help="write the output (for bit-exact A/B checks)")
 a = p.parse_args()
 dev = torch.device("cuda", 0)
 n = -(-a.L // a.b)
@@ -40,3 +41,5 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.iters
 knobs = " ".join(f"{k}={os.environ[k]}" for k in sorted(os.environ) if k.startswith("STAR_K1_"))
 print(f"{knobs or 'defaults'} ms={ms:.2f} TFLOP/s={flops / ms / 1e9:.1f}")
+if a.save:
+    torch.save(out.cpu(), a.save)
