@@ -60,6 +60,7 @@ def _write(ops, caches):
     (3, [4096, 1000, 2500], 32, 8, 128, 0),    # Llama-8B heads, auto splits (fix-up pushes)
     (4, [700, 0, 3000, 64], 8, 2, 64, 1),      # one split per group (epilogue pushes), empty rank
     (2, [20000, 9000], 8, 8, 128, 0),
+    (8, [16384, 9000, 16384, 0, 5000, 16384, 700, 16384], 32, 8, 128, 0),  # a full node
 ])
 def test_exchange_matches_unfused_and_oracle(mods, dtype, world, lens, hq, hkv, d, splits):
     ops, D = mods
@@ -160,7 +161,7 @@ def test_exchange_rejects_oversized_call(mods):
         exs[0].push(o, s, 1, 4, 4, 2)
 
 
-@pytest.mark.parametrize("world,splits", [(1, 0), (3, 2), (2, 3)])
+@pytest.mark.parametrize("world,splits", [(1, 0), (3, 2), (2, 3), (8, 2)])
 def test_fused_exchange_one_kernel(mods, world, splits):
     """star_phase2_exchange: partial + push + cross-rank merge in ONE K2 launch per rank
     (co-resident word-mode grid).  Ranks run on separate streams of one GPU with small grids
@@ -168,7 +169,7 @@ def test_fused_exchange_one_kernel(mods, world, splits):
     against the unfused K2 + K3 merge, and against plain K2 for one rank."""
     ops, D = mods
     hq, hkv, d, ps = 8, 2, 128, 64
-    lens = [2000, 1500, 2600][:world]
+    lens = [2000, 1500, 2600, 900, 3100, 1700, 2222, 1300][:world]
     caches = _rank_caches(lens, hkv, d, torch.bfloat16, ps, seed=21 + world)
     _write(ops, caches)
     exs = D.local_peer_exchanges(world, 4 * hq, hkv, d, "cuda")
