@@ -749,15 +749,29 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     }
   }
   const bool keysplit = QR <= 16;
+  // Word mode spins on other CTAs of the grid, so it is launched COOPERATIVELY: the driver
+  // guarantees every CTA co-resident (also against kernels on other streams), and refuses the
+  // launch instead of deadlocking if the grid cannot fit.
 #define STAR_P2M(DD, KS)                                                                        \
   do {                                                                                          \
     auto kern = phase2_mma_kernel<DD, KS>;                                                      \
     const int bytes = Smem<DD>::kBytes;                                                         \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \
-    kern<<<grid, Cons<KS>::kThreads, bytes, s>>>(tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, \
-                                       pps, page_size, kv_len, own_tail, chunk, out, lse, part_rows, \
-                                       sl2, final_out, final_lse, counters, grp_epoch, pp);      \
+    cudaLaunchAttribute attr[1];                                                                \
+    attr[0].id = cudaLaunchAttributeCooperative;                                                \
+    attr[0].val.cooperative = 1;                                                                \
+    cudaLaunchConfig_t cfg = {};                                                                \
+    cfg.gridDim = grid;                                                                         \
+    cfg.blockDim = dim3(Cons<KS>::kThreads);                                                    \
+    cfg.dynamicSmemBytes = bytes;                                                               \
+    cfg.stream = s;                                                                             \
+    cfg.attrs = attr;                                                                           \
+    cfg.numAttrs = grp_epoch != nullptr ? 1 : 0;                                                \
+    e = cudaLaunchKernelEx(&cfg, kern, tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, pps, \
+                           page_size, kv_len, own_tail, chunk, out, lse, part_rows, sl2,        \
+                           final_out, final_lse, counters, grp_epoch, pp);                      \
+    if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 launch: %s", cudaGetErrorString(e));  \
   } while (0)
   if (d == 128) {
     if (keysplit) STAR_P2M(128, true); else STAR_P2M(128, false);
