@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kXWarps * 32) exchange_merge_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * (int64_t)kXWarps + warp;
   uint32_t* hdr = L.header(box);
-  const uint32_t epoch = __ldcg(hdr) + 1u;
+  const uint32_t epoch = next_epoch(__ldcg(hdr));
   const int par = (int)(epoch & 1u);
   const int d = L.d;
   if (row < nrows) {

@@ -92,8 +92,14 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 
 // epoch of the exchange in flight (completed exchanges of this rank + 1; kernel-boundary
 // ordered after the previous K3x, which advanced the counter)
+// Successor of an epoch counter: 0 (the value of a zeroed word) is never used, and the
+// parity still alternates across the 32-bit wrap (0xFFFFFFFF -> 2).
+__device__ __forceinline__ uint32_t next_epoch(uint32_t c) {
+  const uint32_t e = c + 1u;
+  return e == 0u ? 2u : e;
+}
 __device__ __forceinline__ uint32_t exchange_epoch(const PeerPush& pp) {
-  return __ldcg(pp.L.header(pp.box[pp.rank])) + 1u;
+  return next_epoch(__ldcg(pp.L.header(pp.box[pp.rank])));
 }
 
 // final partial element stores: the local arrays (local_only, e.g. a split partial that the

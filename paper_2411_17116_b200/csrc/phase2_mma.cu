@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   const uint32_t ep = (gridDim.x == 1 && pp.L.world > 0) ? exchange_epoch(pp) : 0u;
   // word-mode split fix-up: this split's partial goes out as {value, epoch} words
   const bool words = grp_epoch != nullptr && gridDim.x > 1;
-  const uint32_t es = words ? __ldcg(grp_epoch + b * gridDim.y + kvh) + 1u : 0u;
+  const uint32_t es = words ? next_epoch(__ldcg(grp_epoch + b * gridDim.y + kvh)) : 0u;
   uint2* const w_out = reinterpret_cast<uint2*>(out);
   uint2* const w_lse = w_out + (int64_t)gridDim.x * part_stride_rows * D;
   uint2* const wsp_out = w_out + (int64_t)split * part_stride_rows * D;

@@ -201,3 +201,53 @@ def test_fused_exchange_one_kernel(mods, world, splits):
             o, s = outs[r]
             assert torch.equal(o.view(lq * hq, d), ref), (lq, r)
             assert torch.equal(s.view(lq * hq), ref_lse), (lq, r)
+
+
+def test_epoch_counters_wrap(mods):
+    """Box and word-mode epochs across the 32-bit wrap (0xFFFFFFFE -> 0xFFFFFFFF -> 2 -> 3):
+    0 is skipped (it is the value of a zeroed word) and the parity keeps alternating."""
+    ops, D = mods
+    hq, hkv, d, ps = 8, 2, 128, 64
+    caches = _rank_caches([3000, 2000], hkv, d, torch.bfloat16, ps, seed=77)
+    _write(ops, caches)
+    # two ranks in one process: the two-kernel path (K2 push + K3x); one rank: the one-kernel path
+    for world in (2, 1):
+        exs = D.local_peer_exchanges(world, hq, hkv, d, "cuda")
+        for ex in exs:
+            ex.own_box.view(torch.int32)[0] = -2  # 0xFFFFFFFE completed exchanges
+        ws = [ops.Phase2Workspace() for _ in range(world)]
+        g = torch.Generator().manual_seed(1)
+        for step in range(4):
+            q = torch.randn(1, 1, hq, d, generator=g).to(torch.bfloat16).cuda()
+            parts = []
+            for r in range(world):
+                k, v, kp, vp, table = caches[r]
+                kv_len = torch.tensor([k.shape[0]], dtype=torch.int32, device="cuda")
+                if step == 0:  # push the word-mode group epochs to the wrap too
+                    ops.phase2_partial(q, kp, vp, table.view(1, -1), kv_len, k.shape[0],
+                                       workspace=ws[r])
+                    torch.cuda.synchronize()
+                    hdr = ws[r].buf.view(torch.int32)
+                    hdr[2048:2048 + hkv] = -2
+                o, s = ops.phase2_partial(q, kp, vp, table.view(1, -1), kv_len, k.shape[0],
+                                          workspace=ops.Phase2Workspace())
+                parts.append((o.view(hq, d), s.view(hq)))
+                if world == 2:
+                    exs[r].push_partial(q, kp, vp, table.view(1, -1), kv_len, k.shape[0],
+                                        workspace=ws[r])
+            if world == 2:
+                ref, ref_lse = ops.merge(torch.stack([p[0] for p in parts]),
+                                         torch.stack([p[1] for p in parts]))
+                for r in range(world):
+                    out, lse = exs[r].merge(1, 1, hq, hkv)
+                    assert torch.equal(out, ref) and torch.equal(lse, ref_lse), (world, step, r)
+            else:
+                k, v, kp, vp, table = caches[0]
+                kv_len = torch.tensor([k.shape[0]], dtype=torch.int32, device="cuda")
+                out, lse = exs[0].exchange(q, kp, vp, table.view(1, -1), kv_len, k.shape[0],
+                                           workspace=ws[0])
+                assert torch.equal(out.view(hq, d), parts[0][0]), (world, step)
+                assert torch.equal(lse.view(hq), parts[0][1]), (world, step)
+        torch.cuda.synchronize()
+        hdr0 = int(exs[0].own_box.view(torch.int32)[0].item()) & 0xFFFFFFFF
+        assert hdr0 == 4, hdr0  # 0xFFFFFFFF, 2, 3, 4
