@@ -431,7 +431,11 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
   if (q_dtype != kv_dtype) return fail(STAR_ENOTSUP, "phase2: q and kv dtypes must match");
   if (d != 64 && d != 128 && d != 32 && d != 16)
     return fail(STAR_ENOTSUP, "phase2: head_dim %d not in {16,32,64,128}", d);
-  if (n_splits <= 0) n_splits = phase2_auto_splits(batch, hkv, max_kv_len, page_size);
+  // the tensor-core path runs G*lq > 16 query rows as 64-row blocks along grid.y: one wave
+  // counts every row block as a group
+  const int qrows = (hq / hkv) * lq;
+  const int n_rb = qrows <= 16 ? 1 : (qrows + 63) / 64;
+  if (n_splits <= 0) n_splits = phase2_auto_splits(batch, hkv * n_rb, max_kv_len, page_size);
   int64_t chunk = std::max<int64_t>(1, (max_kv_len + n_splits - 1) / n_splits);
   const int TN = kv_dtype == STAR_BF16 ? 64 : 32;
   chunk = (chunk + TN - 1) / TN * TN;
@@ -453,8 +457,8 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
   int64_t rows = (int64_t)batch * lq * hq;
   if (n_splits > 1) {
     if (workspace == nullptr) return fail(STAR_ECONFIG, "phase2: workspace required for splits");
-    if ((int64_t)batch * hkv > kEpochOffsetWords)
-      return fail(STAR_ENOTSUP, "phase2: batch x kv heads > %d", kEpochOffsetWords);
+    if ((int64_t)batch * hkv * n_rb > kEpochOffsetWords)
+      return fail(STAR_ENOTSUP, "phase2: batch x kv heads x row blocks > %d", kEpochOffsetWords);
     po = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + kCounterBytes);
     pl = po + (int64_t)n_splits * rows * d;
   }

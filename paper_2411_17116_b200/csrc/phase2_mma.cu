@@ -111,26 +111,26 @@ __device__ __forceinline__ void k2_tr(int slot) {
 // and loads the lse and out of 16 splits for both at once (64 loads in flight), folding
 // further groups of 16 splits, if any, online (running max, as the kernel's tile fold).
 template <int D, int NT>
-__device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq, int G,
+__device__ void split_fixup(unsigned char* smem, int b, int kvh, int r_lo, int r_n, int lq,
+                            int hq, int G,
                             const float* ws_out, const float* ws_lse, int64_t part_rows,
                             float* final_out, float* final_lse, int* counters,
                             const PeerPush& pp) {
   constexpr int PS = 16;  // splits per load round
   const int tid = threadIdx.x;
   const int nsp = gridDim.x;
-  const int QR = G * lq;
   int* flag = reinterpret_cast<int*>(smem);
   named_barrier_sync(1, NT);  // every consumer's partial stores precede thread 0's release
   if (tid == 0) {
     __threadfence();
-    const int old = atomicAdd(&counters[b * gridDim.y + kvh], 1);
+    const int old = atomicAdd(&counters[b * gridDim.y + blockIdx.y], 1);
     __threadfence();
     *flag = (old == nsp - 1);
   }
   named_barrier_sync(1, NT);
   if (!*flag) return;
   const uint32_t ep = pp.L.world ? exchange_epoch(pp) : 0u;
-  for (int e0 = tid; e0 < QR * D; e0 += 2 * NT) {
+  for (int e0 = tid; e0 < r_n * D; e0 += 2 * NT) {
     int64_t orow[2];
     int c[2];
     bool ok[2];
@@ -138,8 +138,8 @@ __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq,
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int e = e0 + k * NT;
-      ok[k] = e < QR * D;
-      const int rr = (ok[k] ? e : 0) / D;
+      ok[k] = e < r_n * D;
+      const int rr = r_lo + (ok[k] ? e : 0) / D;
       c[k] = (ok[k] ? e : 0) % D;
       orow[k] = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
     }
@@ -180,7 +180,7 @@ __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq,
                 acc[k] > 0.f ? m[k] + __logf(acc[k]) : -INFINITY);
     }
   }
-  if (tid == 0) counters[b * gridDim.y + kvh] = 0;  // re-arm for the next launch
+  if (tid == 0) counters[b * gridDim.y + blockIdx.y] = 0;  // re-arm for the next launch
 }
 
 // The whole peer exchange inside K2 (pp.merge; word mode, so every CTA of every rank is
@@ -190,13 +190,14 @@ __device__ void split_fixup(unsigned char* smem, int b, int kvh, int lq, int hq,
 // order with the merge rule of merge_partials (fp64 weights, as K3x), writing the merged
 // fp32 out / lse.  The last CTA of the grid to finish advances the box's epoch.
 template <int D, int NT>
-__device__ void exchange_merge_slice(int b, int kvh, int lq, int hq, int G, int lo, int hi,
+__device__ void exchange_merge_slice(int b, int kvh, int r_lo, int lq, int hq, int G, int lo,
+                                     int hi,
                                      uint32_t ep, float* out, float* lse, const PeerPush& pp) {
   void* box = pp.box[pp.rank];
   const int par = (int)(ep & 1u);
   const int world = pp.L.world;
   for (int e = lo + (int)threadIdx.x; e < hi; e += NT) {
-    const int rr = e / D, c = e % D;
+    const int rr = r_lo + e / D, c = e % D;
     const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
     float lv[kMaxPeers], ov[kMaxPeers];
     uint64_t t0 = 0;
@@ -263,21 +264,21 @@ __device__ void exchange_merge_slice(int b, int kvh, int lq, int hq, int G, int 
 // round and spreads the one-CTA merge tail (two load rounds + fold) over the group
 // (tools/k2_trace.py: 16K rows, last split stored -> exit 3.8 us -> see DESIGN §3 K2).
 template <int D, int NT>
-__device__ void split_merge_words(int b, int kvh, int lq, int hq, int G, const uint2* w_out,
+__device__ void split_merge_words(int b, int kvh, int r_lo, int r_n, int lq, int hq, int G,
+                                  const uint2* w_out,
                                   const uint2* w_lse, int64_t part_rows, uint32_t es,
                                   float* final_out, float* final_lse, uint32_t* grp_epoch,
                                   const PeerPush& pp) {
   constexpr int PS = 16;  // splits per load round (16 lse + 16 out words in flight)
   const int tid = threadIdx.x;
   const int nsp = gridDim.x;
-  const int QR = G * lq;
-  const int total = QR * D;
+  const int total = r_n * D;
   const int per = (total + nsp - 1) / nsp;
   const int lo = blockIdx.x * per, hi = min(total, lo + per);
   named_barrier_sync(1, NT);  // this CTA's own words are visible to its polls
   const uint32_t ep = (pp.L.world && lo < hi) ? exchange_epoch(pp) : 0u;
   for (int e = lo + tid; e < hi; e += NT) {
-    const int rr = e / D, c = e % D;
+    const int rr = r_lo + e / D, c = e % D;
     const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
     float m = -INFINITY, acc = 0.f, o = 0.f;
     for (int p0 = 0; p0 < nsp; p0 += PS) {
@@ -321,8 +322,9 @@ __device__ void split_merge_words(int b, int kvh, int lq, int hq, int G, const u
   }
   // every split's words were seen, so every CTA of the group has read the epoch: advance it
   // for the next launch (all CTAs of the group store the same value)
-  if (tid == 0) grp_epoch[b * gridDim.y + kvh] = es;
-  if (pp.merge) exchange_merge_slice<D, NT>(b, kvh, lq, hq, G, lo, hi, ep, final_out, final_lse, pp);
+  if (tid == 0) grp_epoch[b * gridDim.y + blockIdx.y] = es;
+  if (pp.merge)
+    exchange_merge_slice<D, NT>(b, kvh, r_lo, lq, hq, G, lo, hi, ep, final_out, final_lse, pp);
 }
 
 template <int D, bool KEYSPLIT>
@@ -344,7 +346,14 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kBarOff);
   uint64_t* empty = full + STAGES;
 
-  const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  // row mode (G*lq > 16 query rows, e.g. a 32-token query encode) splits the group's rows
+  // into 64-row blocks along grid.y, so every K/V tile is streamed once per split (the row
+  // blocks of a split run side by side and share it through L2) instead of once per pass
+  const int QRg = (hq / hkv) * lq;
+  const int n_rb = KEYSPLIT ? 1 : (QRg + 63) / 64;
+  const int split = blockIdx.x, kvh = blockIdx.y / n_rb, rb = blockIdx.y % n_rb, b = blockIdx.z;
+  const int r_lo = KEYSPLIT ? 0 : rb * 64;
+  const int r_n = KEYSPLIT ? QRg : min(64, QRg - r_lo);
   // a programmatic dependent (K3x of the peer exchange, which only polls the words this
   // kernel stores) may launch now and wait on SMs beside us instead of behind a kernel boundary
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -360,7 +369,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   const int32_t* table = page_table + (int64_t)b * pages_per_seq;
   float* out_part = out + (int64_t)split * part_stride_rows * D;
   float* lse_part = lse + (int64_t)split * part_stride_rows;
-  const int n_pass = KEYSPLIT ? 1 : (QR + 63) / 64;
+  const int n_pass = 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -424,7 +433,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   const uint32_t ep = (gridDim.x == 1 && pp.L.world > 0) ? exchange_epoch(pp) : 0u;
   // word-mode split fix-up: this split's partial goes out as {value, epoch} words
   const bool words = grp_epoch != nullptr && gridDim.x > 1;
-  const uint32_t es = words ? next_epoch(__ldcg(grp_epoch + b * gridDim.y + kvh)) : 0u;
+  const uint32_t es = words ? next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y)) : 0u;
   uint2* const w_out = reinterpret_cast<uint2*>(out);
   uint2* const w_lse = w_out + (int64_t)gridDim.x * part_stride_rows * D;
   uint2* const wsp_out = w_out + (int64_t)split * part_stride_rows * D;
@@ -432,7 +441,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
   const int grp = warp >> 2, wq4 = warp & 3;  // tile group, warp within the group
   for (int pass = 0; pass < n_pass; ++pass) {
-    const int qbase = KEYSPLIT ? 0 : pass * 64 + wq4 * 16;  // first q row of this warp
+    const int qbase = KEYSPLIT ? 0 : r_lo + pass * 64 + wq4 * 16;  // first q row of this warp
     // ---- Q A-fragments (16 rows x D) straight from global ----
     uint32_t qa[D / 16][4];
     {
@@ -672,10 +681,10 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   }
   K2_TR(threadIdx.x == 0, 3);
   if (words) {
-    split_merge_words<D, NC * 32>(b, kvh, lq, hq, G, w_out, w_lse, part_stride_rows, es,
+    split_merge_words<D, NC * 32>(b, kvh, r_lo, r_n, lq, hq, G, w_out, w_lse, part_stride_rows, es,
                                   final_out, final_lse, grp_epoch, pp);
   } else if (gridDim.x > 1 && counters != nullptr) {
-    split_fixup<D, NC * 32>(smem, b, kvh, lq, hq, G, out, lse, part_stride_rows, final_out,
+    split_fixup<D, NC * 32>(smem, b, kvh, r_lo, r_n, lq, hq, G, out, lse, part_stride_rows, final_out,
                             final_lse, counters, pp);
   }
   K2_TR(threadIdx.x == 0, 5);
@@ -713,7 +722,8 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   if (n_splits > 1 && (int64_t)n_splits * QR * 4 + QR * 4 + 16 > stage_bytes)
     return fail(STAR_ECONFIG, "phase2: %d splits x %d query rows exceed the fix-up buffer", n_splits,
                 QR);
-  dim3 grid(n_splits, hkv, batch);
+  const int n_rb = QR <= 16 ? 1 : (QR + 63) / 64;  // row blocks (see the kernel)
+  dim3 grid(n_splits, hkv * n_rb, batch);
   // timing experiment only (tools/decode_bench.py): skip the split fix-up (result incomplete)
   static const bool no_fix = getenv("STAR_K2_EXPERIMENT_NOFIX") != nullptr;
   if (no_fix) counters = nullptr;
@@ -723,7 +733,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   static const bool force_atomic = getenv("STAR_K2_FIXUP") != nullptr && getenv("STAR_K2_FIXUP")[0] == 'a';
   uint32_t* grp_epoch = nullptr;
   if (counters != nullptr && n_splits > 1 && !force_atomic &&
-      (int64_t)n_splits * batch * hkv <= num_sms())  // whole grid co-resident (1 CTA / SM)
+      (int64_t)n_splits * batch * hkv * n_rb <= num_sms())  // whole grid co-resident (1 CTA / SM)
     grp_epoch = reinterpret_cast<uint32_t*>(counters) + kEpochOffsetWords;
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)d));
   const int64_t part_rows = (int64_t)batch * lq * hq;

@@ -270,7 +270,11 @@ def _phase2_args(q, k_pages, v_pages, page_table, kv_len, max_kv_len, own_tail, 
         raise ShapeError("page table shorter than max_kv_len")
     lib = _lib.load()
     if n_splits <= 0:
-        n_splits = lib.star_phase2_auto_splits(B, hkv, int(max_kv_len), page_size)
+        # (the tensor-core kernel runs > 16 query rows per kv head as 64-row blocks; one wave
+        # counts each block, as star_phase2_partial does for n_splits = 0)
+        qrows = (hq // hkv) * lq
+        n_rb = 1 if qrows <= 16 else -(-qrows // 64)
+        n_splits = lib.star_phase2_auto_splits(B, hkv * n_rb, int(max_kv_len), page_size)
     if out is None:
         out = torch.empty((B, lq, hq, d), dtype=torch.float32, device=q.device)
     if lse is None:

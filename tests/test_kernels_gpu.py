@@ -186,6 +186,10 @@ def test_kv_write_read_roundtrip(ops):
     (3, 3, 4, 2, 64, [400, 3], 4),
     (5, 0, 8, 8, 64, [1000, 2000], 7),
     (32, 32, 4, 4, 64, [1024 + 32], 0),
+    # > 64 query rows per kv head (32-token query encode at Llama-8B heads): two 64-row
+    # blocks along grid.y; and 80 rows (a partial second block)
+    (32, 32, 32, 8, 128, [5000 + 32, 800], 0),
+    (20, 20, 16, 4, 64, [3000], 3),
     # 19 x 8 = 152 (sequence, kv head) groups >= the SM count: the arrival-counter split
     # fix-up (fewer groups use the word fix-up, where split 0 polls the others' words)
     (1, 0, 8, 8, 64, [300 + 37 * i for i in range(19)], 2),
