@@ -483,6 +483,14 @@ def run_ours(args):
 
     dec_us = time_replays(graph, 200)
     k2_us = time_replays(k2_graph, 5, per=n_k2)
+    # phase-2 query encode (BASELINE configs[0]'s l_q = 32 query tokens at these heads; the
+    # query rank's own-tail mask), informational: K2 over the rank's cache
+    lq_enc = 32
+    q_enc = ops.prng_fill((1, lq_enc, hq, d), seed ^ 5, 1, 1.0, torch.bfloat16, dev)
+    ws_enc = ops.Phase2Workspace()
+    enc_graph = capture(lambda: ops.phase2_partial(q_enc, kpool, vpool, table.view(1, -1), kv_len,
+                                                   own_rows, own_tail=lq_enc, workspace=ws_enc), 5)
+    enc_us = time_replays(enc_graph, 5, per=5)
     kv_bytes = own_rows * hkv * d * 2 * 2
     decode = {
         "us_per_token_per_layer": dec_us, "batch": 1, "context": L,
@@ -502,6 +510,10 @@ def run_ours(args):
                                "overhead over plain K2 at N = 1"),
         "collective_us": coll_us,
         "collective_note": "K2 + NCCL all_gather of packed fp32 (out | lse) + K3, for comparison",
+        "query_encode": {"l_q": lq_enc, "us_per_layer": enc_us, "own_tail": lq_enc,
+                         "note": "phase-2 query encode: K2 over the rank's cache with the query "
+                                 "rank's own-tail causal mask (G*l_q = 128 rows per kv head, "
+                                 "bound by the mma.sync rate, not HBM)"},
     }
 
     if rank != 0:
