@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "sm100.cuh"
+#include "softmax_tc.cuh"
 
 namespace star {
 
@@ -83,247 +84,8 @@ __device__ long long g_k1_trace[2 * kTrTiles * 5 + kTrTiles * 2 * 2];
   do {                   \
   } while (0)
 #endif
+// per-row softmax helpers (row_max, exp_pack, tmem_ld_row128, ...): softmax_tc.cuh
 
-// Softmax pass 1 over one 128-column S row in TMEM: max of the (masked) raw scores.
-// Loads are software-pipelined: chunk c+1 is in flight while chunk c is reduced.
-template <bool DIAG>
-__device__ __forceinline__ float row_max(uint32_t s_tm, int lim) {
-  uint32_t buf[2][32];
-  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-  tmem_ld32(s_tm, buf[0]);
-  tmem_wait_ld_tied(buf[0]);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    if (c < 3) tmem_ld32(s_tm + (c + 1) * 32, buf[(c + 1) & 1]);
-    uint32_t* a = buf[c & 1];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      float v0 = __uint_as_float(a[e]), v1 = __uint_as_float(a[e + 1]);
-      if (DIAG) {
-        if (c * 32 + e > lim) v0 = -INFINITY;
-        if (c * 32 + e + 1 > lim) v1 = -INFINITY;
-      }
-      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(v0, v1));
-    }
-    if (c < 3) tmem_wait_ld_tied(buf[(c + 1) & 1]);
-  }
-  return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-}
-
-// 2^x for a pair on the FMA pipe (offloads the MUFU/XU pipe): x clamped to >= -125,
-// x = n + f with n = round(x) (magic-number rounding), 2^f by a degree-3 minimax
-// polynomial on [-1/2, 1/2] (max rel. error 2.1e-4, below bf16's 2^-9 rounding of P),
-// then n is added to the exponent field with one IMAD.
-__device__ __forceinline__ float2 poly_ex2x2(float2 x) {
-  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-  x.x = fmaxf(x.x, -125.f);
-  x.y = fmaxf(x.y, -125.f);
-  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
-  const float2 r = fadd2(t, make_float2(-kMagic, -kMagic));
-  const float2 f = fadd2(x, make_float2(-r.x, -r.y));
-  float2 p = ffma2(f, make_float2(0.05484800413f, 0.05484800413f),
-                   make_float2(0.24180661142f, 0.24180661142f));
-  p = ffma2(p, f, make_float2(0.69324821234f, 0.69324821234f));
-  p = ffma2(p, f, make_float2(0.99998867512f, 0.99998867512f));
-  return make_float2(__int_as_float(__float_as_int(t.x) * 8388608 + __float_as_int(p.x)),
-                     __int_as_float(__float_as_int(t.y) * 8388608 + __float_as_int(p.y)));
-}
-
-// volatile forms: the compiler keeps their relative (source) order, which here is the
-// latency-hiding schedule (exponentials first, packs after)
-__device__ __forceinline__ float ex2v(float x) {
-  float y;
-  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ uint32_t pack_bf16x2v(float lo, float hi) {
-  uint32_t r;
-  asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-
-// f32 += bf16 (one FHADD.BF16 per element, no unpack): the exact fp32 value of the
-// bf16-rounded p joins the row sum.
-__device__ __forceinline__ void acc_bf16x2(float& lo_acc, float& hi_acc, uint32_t w) {
-  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
-      "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
-      : "+f"(lo_acc), "+f"(hi_acc)
-      : "r"(w));
-}
-
-template <bool DIAG, int POLY, bool FH>
-__device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, float m) {
-  float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
-  uint32_t buf[2][32];
-  tmem_ld32(s_tm, buf[0]);
-  tmem_wait_ld_tied(buf[0]);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    // chunk c+1 loads while chunk c is exponentiated; P of chunk c goes to columns
-    // [16c, 16c+16), all below the columns still being read
-    if (c < 3) tmem_ld32(s_tm + (c + 1) * 32, buf[(c + 1) & 1]);
-    const uint32_t* sv = buf[c & 1];
-    uint32_t pk[16];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      const float2 x = ffma2(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), sc2, nm2);
-      float p0, p1;
-      if (c >= 4 - POLY) {
-        const float2 p = poly_ex2x2(x);
-        p0 = p.x;
-        p1 = p.y;
-      } else {
-        p0 = ex2(x.x);
-        p1 = ex2(x.y);
-      }
-      if (DIAG) {
-        const int col = c * 32 + e;
-        if (col > lim) p0 = 0.f;
-        if (col + 1 > lim) p1 = 0.f;
-      }
-      // the row sum uses the bf16-rounded p that the P.V MMA will see, so numerator and
-      // denominator weight each key identically (a dominant key then carries no error)
-      const uint32_t w = pack_bf16x2(p0, p1);
-      pk[e >> 1] = w;
-      float2& acc = rsum[(e >> 1) & 1];
-      if (FH)
-        acc_bf16x2(acc.x, acc.y, w);
-      else
-        acc = fadd2(acc, make_float2(bf16lo(w), bf16hi(w)));
-    }
-    tmem_st16(s_tm + c * 16, pk);
-    if (c < 3) tmem_wait_ld_tied(buf[(c + 1) & 1]);
-  }
-  return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
-}
-
-// One-pass softmax: the whole 128-column S row is loaded into registers once (four
-// tcgen05.ld in flight together, one wait), reduced to its max, then exponentiated in
-// place — no second TMEM read and a single exposed load latency per tile.
-__device__ __forceinline__ void tmem_ld_row128(uint32_t s_tm, uint32_t (&sv)[4][32]) {
-  tmem_ld32(s_tm, sv[0]);
-  tmem_ld32(s_tm + 32, sv[1]);
-  tmem_ld32(s_tm + 64, sv[2]);
-  tmem_ld32(s_tm + 96, sv[3]);
-  tmem_wait_ld_tied(sv[0]);
-  tmem_wait_ld_tied(sv[1]);
-  tmem_wait_ld_tied(sv[2]);
-  tmem_wait_ld_tied(sv[3]);
-}
-
-template <bool DIAG>
-__device__ __forceinline__ float row_max_regs(const uint32_t (&sv)[4][32], int lim) {
-  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      float v0 = __uint_as_float(sv[c][e]), v1 = __uint_as_float(sv[c][e + 1]);
-      if (DIAG) {
-        if (c * 32 + e > lim) v0 = -INFINITY;
-        if (c * 32 + e + 1 > lim) v1 = -INFINITY;
-      }
-      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(v0, v1));
-    }
-  return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-}
-
-template <bool DIAG, int POLY, bool FH>
-__device__ __forceinline__ float exp_pack_regs(const uint32_t (&sv)[4][32], uint32_t s_tm, int lim,
-                                               float sl2, float m) {
-  float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    // all 32 exponentials of the chunk are issued back to back before any result is
-    // consumed, so the MUFU pipe never idles behind its own latency (in-order issue)
-    float p[32];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      const float2 x = ffma2(make_float2(__uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1])),
-                             sc2, nm2);
-      if (c >= 4 - POLY) {
-        const float2 q = poly_ex2x2(x);
-        p[e] = q.x;
-        p[e + 1] = q.y;
-      } else {
-        p[e] = ex2v(x.x);
-        p[e + 1] = ex2v(x.y);
-      }
-    }
-    uint32_t pk[16];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      float p0 = p[e], p1 = p[e + 1];
-      if (DIAG) {
-        const int col = c * 32 + e;
-        if (col > lim) p0 = 0.f;
-        if (col + 1 > lim) p1 = 0.f;
-      }
-      const uint32_t w = pack_bf16x2v(p0, p1);
-      pk[e >> 1] = w;
-      float2& acc = rsum[(e >> 1) & 1];
-      if (FH)
-        acc_bf16x2(acc.x, acc.y, w);
-      else
-        acc = fadd2(acc, make_float2(bf16lo(w), bf16hi(w)));
-    }
-    tmem_st16(s_tm + c * 16, pk);
-  }
-  return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
-}
-
-// Speculative one-pass softmax (ONEP == 2, tiles after the first): exponentiate against the
-// running max m straight away and take the row max of the raw scores in the same pass (the
-// FMNMX3 work fills issue slots of the MUFU-bound loop instead of a pass before it).  P is
-// packed into registers but NOT stored: the caller stores it unless the new max exceeds m by
-// more than the lazy-rescale threshold — the case in which the two-step kernel uses the new
-// max — and then reloads S (still intact in TMEM) and redoes the exps, so P and the row
-// sums are bit-identical to the two-step form.  Register peak as the one-pass form: each
-// chunk's S registers die as its packed P is born.
-template <bool DIAG, bool FH>
-__device__ __forceinline__ float exp_pack_regs_spec(const uint32_t (&sv)[4][32], int lim,
-                                                    float sl2, float m, float& mraw,
-                                                    uint32_t (&pk)[4][16]) {
-  float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
-  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float p[32];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      float v0 = __uint_as_float(sv[c][e]), v1 = __uint_as_float(sv[c][e + 1]);
-      const float2 x = ffma2(make_float2(v0, v1), sc2, nm2);
-      p[e] = ex2v(x.x);
-      p[e + 1] = ex2v(x.y);
-      if (DIAG) {
-        if (c * 32 + e > lim) v0 = -INFINITY;
-        if (c * 32 + e + 1 > lim) v1 = -INFINITY;
-      }
-      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(v0, v1));
-    }
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      float p0 = p[e], p1 = p[e + 1];
-      if (DIAG) {
-        const int col = c * 32 + e;
-        if (col > lim) p0 = 0.f;
-        if (col + 1 > lim) p1 = 0.f;
-      }
-      const uint32_t w = pack_bf16x2v(p0, p1);
-      pk[c][e >> 1] = w;
-      float2& acc = rsum[(e >> 1) & 1];
-      if (FH)
-        acc_bf16x2(acc.x, acc.y, w);
-      else
-        acc = fadd2(acc, make_float2(bf16lo(w), bf16hi(w)));
-    }
-  }
-  mraw = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-  return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
-}
 
 template <int D, int NQ, int POLY, bool FH, int ONEP>
 __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)

@@ -413,6 +413,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
                int* merged, cudaStream_t s);
 int push_partial(const float* out, const float* lse, int batch, int lq, int hq, int hkv, int d,
                  const PeerPush& pp, cudaStream_t s);
+bool phase2_qe_eligible(int qrows, int d, int page_size);
 
 int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hkv, int d,
                    const void* kp, const void* vp, int kv_dtype, int64_t num_pages,
@@ -434,7 +435,9 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
   // the tensor-core path runs G*lq > 16 query rows as 64-row blocks along grid.y: one wave
   // counts every row block as a group
   const int qrows = (hq / hkv) * lq;
-  const int n_rb = qrows <= 16 ? 1 : (qrows + 63) / 64;
+  // (one packed 128-row tile in the tcgen05 query-encode kernel: no row blocks)
+  const int n_rb = (qrows <= 16 || (kv_dtype == STAR_BF16 && phase2_qe_eligible(qrows, d, page_size)))
+                       ? 1 : (qrows + 63) / 64;
   if (n_splits <= 0) n_splits = phase2_auto_splits(batch, hkv * n_rb, max_kv_len, page_size);
   int64_t chunk = std::max<int64_t>(1, (max_kv_len + n_splits - 1) / n_splits);
   const int TN = kv_dtype == STAR_BF16 ? 64 : 32;

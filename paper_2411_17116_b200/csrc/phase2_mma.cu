@@ -14,6 +14,7 @@
 //   row mode (G*lq > 16, query encode): warp w takes q rows [16w, 16w+16) of a
 //     64-row pass over every key of the tile.
 #include <cudaTypedefs.h>
+#include <limits.h>
 #include <stdlib.h>
 
 #include <array>
@@ -23,6 +24,7 @@
 #include "common.cuh"
 #include "exchange.cuh"
 #include "sm100.cuh"
+#include "softmax_tc.cuh"
 
 namespace star {
 
@@ -690,8 +692,354 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   K2_TR(threadIdx.x == 0, 5);
 }
 
+// ------------------------------------------------------------------ K2q: tcgen05 query encode
+// Phase-2 query encode (ss/sim.py:254-281 with own_tail = l_q; partial_attention on every
+// other host): G*l_q in (16, 128] query rows per (sequence, kv head) — e.g. l_q = 32 at
+// Llama-8B heads — are PACKED into one M = 128 tcgen05 tile (row r = token r/G, head r%G,
+// loaded by one 3-D TMA box {64, G, l_q} per 64-column slab), so every 128-key K/V tile
+// feeds one QK^T and one P.V of M = 128 on the tensor pipe instead of 16-row mma.sync
+// fragments.  Keys come straight from the paged pool (two 64-key TMA boxes per tile through
+// the page table, as K2).  One key range ("split") per CTA; the split partials fold by the
+// word-mode fix-up (split_merge_words), which also pushes / merges the peer exchange.
+// TMEM: S double-buffered (S_a | S_b | O = 384 of 512 columns), so QK^T of tile j+1 runs
+// while the softmax of tile j does.  P goes back over its S buffer as a bf16 hi/lo pair
+// (hi in columns [0,64), lo in [64,128)) and P.V runs on both halves: ≈16 mantissa bits of
+// P, as K2's mma.sync path, which keeps the 2e-3 parity bound (bf16 P alone measured 2.04e-3
+// at 5K keys).  Softmax as K1 (one thread per row = TMEM lane, lazy O rescale); padding rows
+// past G*l_q and keys past the split end or the row's own-tail limit are masked.
+namespace p2q {
+constexpr int BN = 128;                 // keys per tile
+constexpr int kSlab = 128 * 128;        // [128 rows x 64 bf16] SW128 slab
+constexpr int kTile = 2 * kSlab;        // [128 x 128] bf16
+constexpr int KST = 3, VST = 3;
+constexpr int kQOff = 0;
+constexpr int kKOff = kQOff + kTile;
+constexpr int kVOff = kKOff + KST * kTile;
+constexpr int kBarOff = kVOff + VST * kTile;
+constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 2 + 2 + 2;
+constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
+constexpr int kThreads = 192;           // warps 0-3 softmax (TMEM lanes), 4 TMA, 5 MMA
+constexpr int kOCol = 2 * BN;           // O after the two S buffers
+static_assert(kSmem <= 232448, "shared memory budget");
+}  // namespace p2q
+
+// P = hi + lo (both bf16) of 2^(s*sl2 - m) for one 128-column row: hi over S columns
+// [16c, 16c+16), lo over [64+16c, ...) for chunk c; returns the row sum of hi + lo.
+template <bool DIAG>
+__device__ __forceinline__ float exp_pack_hilo(const uint32_t (&sv)[4][32], uint32_t s_tm, int lim,
+                                               float sl2, float m) {
+  float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float p[32];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      const float2 x = ffma2(make_float2(__uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1])),
+                             sc2, nm2);
+      p[e] = ex2v(x.x);
+      p[e + 1] = ex2v(x.y);
+    }
+    uint32_t hi[16], lo[16];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float p0 = p[e], p1 = p[e + 1];
+      if (DIAG) {
+        const int col = c * 32 + e;
+        if (col > lim) p0 = 0.f;
+        if (col + 1 > lim) p1 = 0.f;
+      }
+      const uint32_t wh = pack_bf16x2v(p0, p1);
+      const uint32_t wl = pack_bf16x2v(p0 - bf16lo(wh), p1 - bf16hi(wh));
+      hi[e >> 1] = wh;
+      lo[e >> 1] = wl;
+      float2& acc = rsum[(e >> 1) & 1];
+      acc_bf16x2(acc.x, acc.y, wh);
+      acc_bf16x2(acc.x, acc.y, wl);
+    }
+    tmem_st16(s_tm + c * 16, hi);
+    tmem_st16(s_tm + 64 + c * 16, lo);
+  }
+  return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
+}
+
+__global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
+    const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+    const __grid_constant__ CUtensorMap tm_v, int lq, int hq, int hkv,
+    const int32_t* __restrict__ page_table, int pages_per_seq, int page_size,
+    const int32_t* __restrict__ kv_len, int own_tail, int64_t chunk, uint2* __restrict__ w_out,
+    int64_t part_rows, float scale_log2, float* __restrict__ final_out,
+    float* __restrict__ final_lse, uint32_t* __restrict__ grp_epoch, const PeerPush pp) {
+  using namespace p2q;
+  constexpr int D = 128;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + KST;
+  uint64_t* v_full = k_empty + KST;
+  uint64_t* v_empty = v_full + VST;
+  uint64_t* s_full = v_empty + VST;  // [2]
+  uint64_t* p_full = s_full + 2;     // [2]
+  uint64_t* o_done = p_full + 2;     // every P.V (the rescale waits for the previous one)
+  uint64_t* o_last = o_done + 1;     // the last P.V (the epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_last + 1);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  const int G = hq / hkv;
+  const int QR = G * lq;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t len = kv_len[b];
+  const int64_t r0 = (int64_t)split * chunk;
+  const int64_t r1 = min(len, r0 + chunk);
+  const int64_t tail0 = len - own_tail;
+  const int ntiles = r1 > r0 ? (int)((r1 - r0 + BN - 1) / BN) : 0;
+  const int32_t* table = page_table + (int64_t)b * pages_per_seq;
+  uint2* const w_lse = w_out + (int64_t)gridDim.x * part_rows * D;
+
+  // the Q tile's rows past G*l_q are never loaded: zero them (no garbage in their S rows)
+  for (int e = threadIdx.x; e < kTile / 16; e += kThreads)
+    reinterpret_cast<uint4*>(smem + kQOff)[e] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
+    for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); }
+    mbar_init(o_done, 1);
+    mbar_init(o_last, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  // pool row of the 64-key half `hh` of tile t (a half past the split end re-reads the
+  // tile's first half, whose extra keys the softmax masks)
+  auto key_row = [&](int t, int hh) -> int {
+    int64_t row = r0 + (int64_t)t * BN + hh * 64;
+    if (row >= r1) row = r0 + (int64_t)t * BN;
+    const int32_t page = table[row / page_size];
+    return (int)(((int64_t)page * hkv + kvh) * page_size + row % page_size);
+  };
+
+  if (warp == 4) {
+    if (lane == 0 && ntiles > 0) {
+      // ================= TMA producer: Q once, then K (one tile ahead) and V =================
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      mbar_expect_tx(q_full, 2 * QR * 128);
+      for (int a = 0; a < 2; ++a)
+        tma_load_3d(smem + kQOff + a * kSlab, &tm_q, q_full, a * 64, kvh * G, b * lq);
+      int kt = 0, vt = 0;
+      while (vt < ntiles) {
+        if (kt < ntiles && kt <= vt + 1) {
+          const int st = kt % KST;
+          if (kt >= KST) mbar_wait(&k_empty[st], ((kt / KST) + 1) & 1);
+          mbar_expect_tx(&k_full[st], kTile);
+          for (int hh = 0; hh < 2; ++hh) {
+            const int pr = key_row(kt, hh);
+            for (int a = 0; a < 2; ++a)
+              tma_load_2d(smem + kKOff + st * kTile + a * kSlab + hh * 64 * 128, &tm_k, &k_full[st],
+                          a * 64, pr);
+          }
+          ++kt;
+          continue;
+        }
+        const int st = vt % VST;
+        if (vt >= VST) mbar_wait(&v_empty[st], ((vt / VST) + 1) & 1);
+        mbar_expect_tx(&v_full[st], kTile);
+        for (int hh = 0; hh < 2; ++hh) {
+          const int pr = key_row(vt, hh);
+          for (int a = 0; a < 2; ++a)
+            tma_load_2d(smem + kVOff + st * kTile + a * kSlab + hh * 64 * 128, &tm_v, &v_full[st],
+                        a * 64, pr);
+        }
+        ++vt;
+      }
+    }
+  } else if (warp == 5) {
+    // ================= MMA issuer =================
+    // S(j) -> buffer j%2.  Order: S(0), S(1), then per tile j: P.V(j) (hi + lo halves of the
+    // buffer), S(j+2) into the same buffer (in-order execution: P(j) is consumed first).
+    if (lane == 0 && ntiles > 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, BN, false, false);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
+      const uint32_t q_addr = smem_u32(smem + kQOff);
+      const uint32_t k_addr = smem_u32(smem + kKOff);
+      const uint32_t v_addr = smem_u32(smem + kVOff);
+      auto issue_s = [&](int t) {
+        const int st = t % KST;
+        mbar_wait(&k_full[st], (t / KST) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kSlab + (kk & 3) * 32;
+          const uint64_t ad = umma_desc_sw128(q_addr + off, 16, 1024);
+          const uint64_t bd = umma_desc_sw128(k_addr + st * kTile + off, 16, 1024);
+          umma_bf16_ss(tbase + (t & 1) * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[t & 1]);
+        umma_commit(&k_empty[st]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      if (ntiles > 1) issue_s(1);
+      for (int j = 0; j < ntiles; ++j) {
+        const int vs = j % VST;
+        mbar_wait(&v_full[vs], (j / VST) & 1);
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t pb = tbase + (j & 1) * BN;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            const uint64_t bd = umma_desc_sw128(v_addr + vs * kTile + kk * 16 * 128, kSlab, 1024);
+            umma_bf16_ts(tbase + kOCol, pb + h * 64 + kk * 8, bd, idesc_o,
+                         (j > 0 || h > 0 || kk > 0) ? 1u : 0u);
+          }
+        umma_commit(o_done);
+        if (j == ntiles - 1) umma_commit(o_last);
+        umma_commit(&v_empty[vs]);
+        if (j + 2 < ntiles) issue_s(j + 2);
+      }
+    }
+  } else {
+    // ================= softmax (warps 0-3: row r = TMEM lane) =================
+    const int r = warp * 32 + lane;
+    const int ti = r / G;  // token of this row (rows >= G*l_q are padding)
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t o_tm = tbase + lane_off + kOCol;
+    const float sl2 = scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+    // last visible key of this row relative to the split start (the split end and the row's
+    // own-tail causal limit); padding rows (r >= G*l_q) take no mask at all — their values
+    // only ever reach their own O lanes, which are discarded — so a warp with padding rows
+    // stays on the unmasked path
+    const bool pad = r >= QR;
+    const int last_rel = pad ? INT_MAX / 2 : (int)(min(r1 - 1, tail0 + ti) - r0);
+    for (int j = 0; j < ntiles; ++j) {
+      const uint32_t s_tm = tbase + lane_off + (j & 1) * BN;
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const int64_t base = r0 + (int64_t)j * BN;
+      const int lim = max(-1, min(BN, last_rel - j * BN));  // columns c > lim are invisible
+      const bool masked = __any_sync(0xffffffffu, lim < BN - 1);
+      uint32_t sv[4][32];
+      tmem_ld_row128(s_tm, sv);
+      const float mx = (masked ? row_max_regs<true>(sv, lim) : row_max_regs<false>(sv, lim)) * sl2;
+      float m_use = m_run, alpha = 1.f;
+      const bool need = (j == 0) || (mx > m_run + 8.f);
+      const bool warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
+      if (need) {
+        if (j > 0) alpha = ex2(m_run - mx);
+        m_use = mx;
+      }
+      // rows with no visible key in this split (padding rows, or every key past the row's
+      // own-tail limit): a finite m keeps their exp2 arguments finite
+      if (pad || last_rel < 0) m_use = 0.f;
+      const float rs = masked ? exp_pack_hilo<true>(sv, s_tm, lim, sl2, m_use)
+                              : exp_pack_hilo<false>(sv, s_tm, lim, sl2, m_use);
+      if (r1 - base < BN) {
+        // keys past the split end: their V rows may hold stale (even non-finite) data and
+        // P = 0 must not meet a NaN — zero them once the tile has landed
+        const int valid = (int)(r1 - base);
+        mbar_wait(&v_full[j % VST], (j / VST) & 1);
+        if (r >= valid) {
+          unsigned char* vrow = smem + kVOff + (j % VST) * kTile + r * 128;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              reinterpret_cast<uint4*>(vrow + a * kSlab)[c] = make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async_smem();
+      }
+      if (warp_rescale) {
+        // O must hold P.V(j-1) before it is rescaled: wait for that commit (P.V(j) cannot
+        // have completed yet — it needs this tile's P — so the parity is unambiguous)
+        mbar_wait(o_done, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orr[32];
+          tmem_ld32(o_tm + c * 32, orr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+          tmem_st32(o_tm + c * 32, orr);
+        }
+      }
+      tmem_wait_st();
+      l_run = l_run * alpha + rs;
+      m_run = m_use;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+    }
+    // ---- epilogue: this split's partial of row r as {value, epoch} words ----
+    const uint32_t es = next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y));
+    if (ntiles > 0) {
+      // (not o_done's parity: P.V(ntiles-2) may still be in flight here, two phases behind)
+      mbar_wait(o_last, 0);
+      tc_fence_after();
+    }
+    const bool row_ok = r < QR;
+    const int64_t orow = ((int64_t)b * lq + ti) * hq + kvh * G + r % G;
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    uint2* wo = w_out + (int64_t)split * part_rows * D + orow * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t orr[32];
+      if (ntiles > 0) {
+        tmem_ld32(o_tm + c * 32, orr);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) orr[e] = 0u;
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 2)
+          st_word2(wo + c * 32 + e,
+                   make_float2(__uint_as_float(orr[e]) * inv, __uint_as_float(orr[e + 1]) * inv), es);
+      }
+    }
+    if (row_ok)
+      st_word(w_lse + (int64_t)split * part_rows + orow,
+              l_run > 0.f ? (m_run + __log2f(l_run)) * 0.6931471805599453f : -INFINITY, es);
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 5) tmem_free<512>(tbase);
+  if (warp < 4) {
+    // word-mode fold of the splits (+ the peer exchange push / merge when asked)
+    const uint32_t es = next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y));
+    split_merge_words<D, 128>(b, kvh, 0, QR, lq, hq, G, w_out, w_lse, part_rows, es, final_out,
+                              final_lse, grp_epoch, pp);
+  }
+}
+
 // ------------------------------------------------------------------ host
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+
+// K2q (tcgen05 query encode) takes 16 < G*l_q <= 128 packed rows at head_dim 128 over a pool
+// of 64-key-aligned pages; STAR_K2_QE=0 turns it off (measurement)
+bool phase2_qe_eligible(int qrows, int d, int page_size) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("STAR_K2_QE");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on && d == 128 && qrows > 16 && qrows <= 128 && page_size % 64 == 0;
+}
 
 int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const void* kp,
                const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
@@ -722,7 +1070,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   if (n_splits > 1 && (int64_t)n_splits * QR * 4 + QR * 4 + 16 > stage_bytes)
     return fail(STAR_ECONFIG, "phase2: %d splits x %d query rows exceed the fix-up buffer", n_splits,
                 QR);
-  const int n_rb = QR <= 16 ? 1 : (QR + 63) / 64;  // row blocks (see the kernel)
+  int n_rb = QR <= 16 ? 1 : (QR + 63) / 64;  // row blocks (see the kernel)
   dim3 grid(n_splits, hkv * n_rb, batch);
   // timing experiment only (tools/decode_bench.py): skip the split fix-up (result incomplete)
   static const bool no_fix = getenv("STAR_K2_EXPERIMENT_NOFIX") != nullptr;
@@ -732,9 +1080,19 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   // starve one that has not started; else the arrival-counter fix-up.  STAR_K2_FIXUP=atomic forces the latter (measurement).
   static const bool force_atomic = getenv("STAR_K2_FIXUP") != nullptr && getenv("STAR_K2_FIXUP")[0] == 'a';
   uint32_t* grp_epoch = nullptr;
-  if (counters != nullptr && n_splits > 1 && !force_atomic &&
-      (int64_t)n_splits * batch * hkv * n_rb <= num_sms())  // whole grid co-resident (1 CTA / SM)
-    grp_epoch = reinterpret_cast<uint32_t*>(counters) + kEpochOffsetWords;
+  // the tcgen05 query-encode kernel (K2q) for 16 < G*l_q <= 128 packed rows; it needs the
+  // word-mode fix-up (co-resident grid), else the mma.sync row blocks run
+  bool use_qe = false;
+  if (counters != nullptr && n_splits > 1 && !force_atomic) {
+    if (phase2_qe_eligible(QR, d, page_size) && (int64_t)n_splits * batch * hkv <= num_sms()) {
+      use_qe = true;
+      n_rb = 1;
+      grid = dim3(n_splits, hkv, batch);
+      grp_epoch = reinterpret_cast<uint32_t*>(counters) + kEpochOffsetWords;
+    } else if ((int64_t)n_splits * batch * hkv * n_rb <= num_sms()) {  // 1 CTA / SM
+      grp_epoch = reinterpret_cast<uint32_t*>(counters) + kEpochOffsetWords;
+    }
+  }
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)d));
   const int64_t part_rows = (int64_t)batch * lq * hq;
   // the in-kernel cross-rank merge needs the co-resident word-mode grid
@@ -748,7 +1106,8 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     // shape or mode changes (stream-ordered; once per change, e.g. query encode -> decode).
     static std::mutex mu;
     static std::unordered_map<const void*, std::array<int64_t, 6>> last;
-    const std::array<int64_t, 6> sig = {batch, lq, hq, hkv, d, grp_epoch != nullptr};
+    const std::array<int64_t, 6> sig = {batch, lq, hq, hkv, d,
+                                        (grp_epoch != nullptr ? 1 : 0) + (use_qe ? 2 : 0)};
     std::lock_guard<std::mutex> lock(mu);
     auto it = last.find(counters);
     if (it == last.end() || it->second != sig) {
@@ -757,6 +1116,37 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
       if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 workspace reset: %s", cudaGetErrorString(e));
       last[counters] = sig;
     }
+  }
+  if (use_qe) {
+    // Q as [batch*lq rows][hq][d]: one box {64, G, lq} per 64-column slab = the packed tile
+    CUtensorMap tq;
+    const int G = hq / hkv;
+    cuuint64_t qdims[3] = {(cuuint64_t)d, (cuuint64_t)hq, (cuuint64_t)batch * lq};
+    cuuint64_t qstr[2] = {(cuuint64_t)d * 2, (cuuint64_t)hq * d * 2};
+    cuuint32_t qbox[3] = {64, (cuuint32_t)G, (cuuint32_t)lq};
+    cuuint32_t qestr[3] = {1, 1, 1};
+    if (fn(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q), qdims, qstr, qbox,
+           qestr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(STAR_ECUDA, "phase2 query encode: Q tensor map encode failed");
+    cudaError_t e = cudaFuncSetAttribute(phase2_qe_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, p2q::kSmem);
+    if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 qe smem attr: %s", cudaGetErrorString(e));
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(p2q::kThreads);
+    cfg.dynamicSmemBytes = p2q::kSmem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, phase2_qe_kernel, tq, tk, tv, lq, hq, hkv, table, pps, page_size,
+                           kv_len, own_tail, chunk, reinterpret_cast<uint2*>(out), part_rows, sl2,
+                           final_out, final_lse, grp_epoch, pp);
+    if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 qe launch: %s", cudaGetErrorString(e));
+    return STAR_OK;
   }
   const bool keysplit = QR <= 16;
   // Word mode spins on other CTAs of the grid, so it is launched COOPERATIVELY: the driver

@@ -8,6 +8,7 @@ on failure.  No operator has a CPU path: a non-CUDA tensor is an error.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Sequence
 
 import torch
@@ -273,7 +274,9 @@ def _phase2_args(q, k_pages, v_pages, page_table, kv_len, max_kv_len, own_tail, 
         # (the tensor-core kernel runs > 16 query rows per kv head as 64-row blocks; one wave
         # counts each block, as star_phase2_partial does for n_splits = 0)
         qrows = (hq // hkv) * lq
-        n_rb = 1 if qrows <= 16 else -(-qrows // 64)
+        qe = (q.dtype == torch.bfloat16 and d == 128 and 16 < qrows <= 128 and page_size % 64 == 0
+              and os.environ.get("STAR_K2_QE", "1")[:1] != "0")  # tcgen05 query encode: 1 tile
+        n_rb = 1 if (qrows <= 16 or qe) else -(-qrows // 64)
         n_splits = lib.star_phase2_auto_splits(B, hkv * n_rb, int(max_kv_len), page_size)
     if out is None:
         out = torch.empty((B, lq, hq, d), dtype=torch.float32, device=q.device)

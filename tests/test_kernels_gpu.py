@@ -190,6 +190,11 @@ def test_kv_write_read_roundtrip(ops):
     # blocks along grid.y; and 80 rows (a partial second block)
     (32, 32, 32, 8, 128, [5000 + 32, 800], 0),
     (20, 20, 16, 4, 64, [3000], 3),
+    # bf16 d=128, 16 < G*l_q <= 128: the tcgen05 query-encode kernel (packed M=128 tile)
+    (8, 8, 32, 8, 128, [3000, 64], 0),
+    (17, 0, 32, 8, 128, [4000], 5),
+    (5, 5, 16, 4, 128, [700], 0),
+    (32, 32, 32, 8, 128, [130], 2),
     # 19 x 8 = 152 (sequence, kv head) groups >= the SM count: the arrival-counter split
     # fix-up (fewer groups use the word fix-up, where split 0 polls the others' words)
     (1, 0, 8, 8, 64, [300 + 37 * i for i in range(19)], 2),

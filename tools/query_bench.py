@@ -11,14 +11,14 @@ if os.environ.get("STAR_LIB_PATH"):  # A/B against another build
 from paper_2411_17116_b200 import ops  # noqa: E402
 
 dev = torch.device("cuda", 0)
-hq, hkv, d, ps = 32, 8, 128, 128
-for rows in (16384, 131072):
+hq, hkv, d, ps = int(os.environ.get('QB_HQ', 32)), 8, 128, 128
+for rows in [int(x) for x in os.environ.get("QB_ROWS", "16384,131072").split(",")]:
     pages = rows // ps
     kp = ops.prng_fill((pages, hkv, ps, d), 2, 1, 1.0, torch.bfloat16, dev)
     vp = ops.prng_fill((pages, hkv, ps, d), 3, 1, 1.0, torch.bfloat16, dev)
     table = torch.arange(pages, dtype=torch.int32, device=dev).view(1, -1)
     kv_len = torch.tensor([rows], dtype=torch.int32, device=dev)
-    for lq in (1, 4, 16, 32):
+    for lq in [int(x) for x in os.environ.get("QB_LQ", "1,4,16,32").split(",")]:
         q = ops.prng_fill((1, lq, hq, d), 4, 1, 1.0, torch.bfloat16, dev)
         ws = ops.Phase2Workspace()
         f = lambda: ops.phase2_partial(q, kp, vp, table, kv_len, rows, own_tail=lq, workspace=ws)  # noqa
