@@ -56,21 +56,23 @@ def _write(ops, caches):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-@pytest.mark.parametrize("world,lens,hq,hkv,d,splits", [
-    (3, [4096, 1000, 2500], 32, 8, 128, 0),    # Llama-8B heads, auto splits (fix-up pushes)
-    (4, [700, 0, 3000, 64], 8, 2, 64, 1),      # one split per group (epilogue pushes), empty rank
-    (2, [20000, 9000], 8, 8, 128, 0),
-    (8, [16384, 9000, 16384, 0, 5000, 16384, 700, 16384], 32, 8, 128, 0),  # a full node
+@pytest.mark.parametrize("world,lens,hq,hkv,d,splits,lq_query", [
+    # l_q = 32 at Llama-8B heads: the query encode runs on the tcgen05 K2q kernel
+    (3, [4096, 1000, 2500], 32, 8, 128, 0, 32),
+    (3, [4096, 1000, 2500], 32, 8, 128, 0, 4),    # Llama-8B heads, auto splits (fix-up pushes)
+    (4, [700, 0, 3000, 64], 8, 2, 64, 1, 4),      # one split per group (epilogue pushes), empty rank
+    (2, [20000, 9000], 8, 8, 128, 0, 4),
+    (8, [16384, 9000, 16384, 0, 5000, 16384, 700, 16384], 32, 8, 128, 0, 4),  # a full node
 ])
-def test_exchange_matches_unfused_and_oracle(mods, dtype, world, lens, hq, hkv, d, splits):
+def test_exchange_matches_unfused_and_oracle(mods, dtype, world, lens, hq, hkv, d, splits,
+                                             lq_query):
     ops, D = mods
     page_size = 64
     caches = _rank_caches(lens, hkv, d, dtype, page_size, seed=world * 7 + hq)
     _write(ops, caches)
-    lq_query = 4
     exs = D.local_peer_exchanges(world, lq_query * hq, hkv, d, "cuda")
     g = torch.Generator().manual_seed(5)
-    # a 4-row query encode (own tail on the last rank), then two 1-row decode steps
+    # a query encode (own tail on the last rank), then two 1-row decode steps
     for step, (lq, tail) in enumerate([(lq_query, lq_query), (1, 0), (1, 0)]):
         q = torch.randn(1, lq, hq, d, generator=g).to(dtype)
         qd = q.cuda()
@@ -161,21 +163,23 @@ def test_exchange_rejects_oversized_call(mods):
         exs[0].push(o, s, 1, 4, 4, 2)
 
 
-@pytest.mark.parametrize("world,splits", [(1, 0), (3, 2), (2, 3), (8, 2)])
-def test_fused_exchange_one_kernel(mods, world, splits):
+@pytest.mark.parametrize("world,splits,hq,hkv,lq_q", [(1, 0, 8, 2, 4), (3, 2, 8, 2, 4),
+                                                    (2, 3, 8, 2, 4), (8, 2, 8, 2, 4),
+                                                    (2, 2, 32, 8, 32), (1, 0, 32, 8, 32)])
+def test_fused_exchange_one_kernel(mods, world, splits, hq, hkv, lq_q):
     """star_phase2_exchange: partial + push + cross-rank merge in ONE K2 launch per rank
     (co-resident word-mode grid).  Ranks run on separate streams of one GPU with small grids
     (world x splits x hkv CTAs all resident), as they would on separate GPUs; bit-exact
     against the unfused K2 + K3 merge, and against plain K2 for one rank."""
     ops, D = mods
-    hq, hkv, d, ps = 8, 2, 128, 64
+    d, ps = 128, 64
     lens = [2000, 1500, 2600, 900, 3100, 1700, 2222, 1300][:world]
     caches = _rank_caches(lens, hkv, d, torch.bfloat16, ps, seed=21 + world)
     _write(ops, caches)
-    exs = D.local_peer_exchanges(world, 4 * hq, hkv, d, "cuda")
+    exs = D.local_peer_exchanges(world, lq_q * hq, hkv, d, "cuda")
     streams = [torch.cuda.Stream() for _ in range(world)]
     g = torch.Generator().manual_seed(3)
-    for lq, tail in ((4, 4), (1, 0), (1, 0)):
+    for lq, tail in ((lq_q, lq_q), (1, 0), (1, 0)):
         q = torch.randn(1, lq, hq, d, generator=g).to(torch.bfloat16).cuda()
         torch.cuda.synchronize()
         outs = [None] * world
