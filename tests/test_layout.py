@@ -161,3 +161,21 @@ def test_context_layout_copy_plan(G, rank):
             filled[r0:r0 + m] = filled[src:src + m]
     assert (filled == pos).all()
     assert h2d_rows == n_ctx
+
+
+def test_pipeline_cut_points():
+    """Host logic of the e2e pipeline's causal parts (pipeline._cuts): whole 128-row q tiles,
+    sorted, covering [0, m); only the first and last segments are split."""
+    from paper_2411_17116_b200 import pipeline
+
+    for m in (16384, 32768, 1000, 130):
+        for first in (False, True):
+            for last in (False, True):
+                cuts = pipeline._cuts(m, first, last)
+                assert cuts[0] == 0 and cuts[-1] == m
+                assert cuts == sorted(set(cuts))
+                assert all(c % 128 == 0 for c in cuts[:-1])
+                if not first and not last:
+                    assert cuts == [0, m]
+    assert pipeline._cuts(16384, True, False) == [0, 8192, 16384]
+    assert pipeline._cuts(32768, False, True) == [0, 16384, 24576, 32768]
