@@ -474,7 +474,9 @@ def run_ours(args):
                                                   own_rows, workspace=ws), n_k2)
     exch_us = time_replays(capture(peer_step), 200)
     coll_us = None
-    if world > 1:
+    if world > 1 and backend != "nccl":
+        coll_us = f"unmeasured ({backend} collectives cannot be graph-captured)"
+    elif world > 1:
         try:
             coll_us = time_replays(capture(collective_step), 200)
         except Exception as exc:  # a backend without graph capture
