@@ -195,6 +195,8 @@ def test_kv_write_read_roundtrip(ops):
     (17, 0, 32, 8, 128, [4000], 5),
     (5, 5, 16, 4, 128, [700], 0),
     (32, 32, 32, 8, 128, [130], 2),
+    # G*l_q = 160 > 128: mma.sync row blocks (64 + 64 + 32 rows) at d = 128
+    (40, 40, 32, 8, 128, [2000], 0),
     # 19 x 8 = 152 (sequence, kv head) groups >= the SM count: the arrival-counter split
     # fix-up (fewer groups use the word fix-up, where split 0 polls the others' words)
     (1, 0, 8, 8, 64, [300 + 37 * i for i in range(19)], 2),
