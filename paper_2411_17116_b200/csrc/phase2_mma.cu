@@ -984,8 +984,11 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j & 1]);
     }
-    // ---- epilogue: this split's partial of row r as {value, epoch} words ----
-    const uint32_t es = next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y));
+    // ---- epilogue: this split's partial of row r as {value, epoch} words; with one split
+    // (no fold) the final partial itself — local, or pushed to every rank's box ----
+    const bool single = gridDim.x == 1;
+    const uint32_t es = single ? 0u : next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y));
+    const uint32_t ep = (single && pp.L.world > 0) ? exchange_epoch(pp) : 0u;
     if (ntiles > 0) {
       // (not o_done's parity: P.V(ntiles-2) may still be in flight here, two phases behind)
       mbar_wait(o_last, 0);
@@ -1007,19 +1010,28 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       }
       if (row_ok) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2)
-          st_word2(wo + c * 32 + e,
-                   make_float2(__uint_as_float(orr[e]) * inv, __uint_as_float(orr[e + 1]) * inv), es);
+        for (int e = 0; e < 32; e += 2) {
+          const float2 v2 =
+              make_float2(__uint_as_float(orr[e]) * inv, __uint_as_float(orr[e + 1]) * inv);
+          if (single)
+            put_out2(pp, ep, false, final_out, orow * D + c * 32 + e, v2);
+          else
+            st_word2(wo + c * 32 + e, v2, es);
+        }
       }
     }
-    if (row_ok)
-      st_word(w_lse + (int64_t)split * part_rows + orow,
-              l_run > 0.f ? (m_run + __log2f(l_run)) * 0.6931471805599453f : -INFINITY, es);
+    if (row_ok) {
+      const float lv = l_run > 0.f ? (m_run + __log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+      if (single)
+        put_lse(pp, ep, false, final_lse, orow, lv);
+      else
+        st_word(w_lse + (int64_t)split * part_rows + orow, lv, es);
+    }
     tc_fence_before();
   }
   __syncthreads();
   if (warp == 5) tmem_free<512>(tbase);
-  if (warp < 4) {
+  if (warp < 4 && gridDim.x > 1) {
     // word-mode fold of the splits (+ the peer exchange push / merge when asked)
     const uint32_t es = next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y));
     split_merge_words<D, 128>(b, kvh, 0, QR, lq, hq, G, w_out, w_lse, part_rows, es, final_out,
@@ -1092,6 +1104,11 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     } else if ((int64_t)n_splits * batch * hkv * n_rb <= num_sms()) {  // 1 CTA / SM
       grp_epoch = reinterpret_cast<uint32_t*>(counters) + kEpochOffsetWords;
     }
+  } else if (n_splits == 1 && phase2_qe_eligible(QR, d, page_size)) {
+    // one split per (sequence, kv head): K2q writes the final partial, no fold (any grid)
+    use_qe = true;
+    n_rb = 1;
+    grid = dim3(1, hkv, batch);
   }
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)d));
   const int64_t part_rows = (int64_t)batch * lq * hq;
@@ -1141,7 +1158,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     cfg.dynamicSmemBytes = p2q::kSmem;
     cfg.stream = s;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = grp_epoch != nullptr ? 1 : 0;  // cooperative only for the word-mode fold
     e = cudaLaunchKernelEx(&cfg, phase2_qe_kernel, tq, tk, tv, lq, hq, hkv, table, pps, page_size,
                            kv_len, own_tail, chunk, reinterpret_cast<uint2*>(out), part_rows, sl2,
                            final_out, final_lse, grp_epoch, pp);

@@ -195,6 +195,8 @@ def test_kv_write_read_roundtrip(ops):
     (17, 0, 32, 8, 128, [4000], 5),
     (5, 5, 16, 4, 128, [700], 0),
     (32, 32, 32, 8, 128, [130], 2),
+    # batch 10 x 8 kv heads = 80 groups: one split each, K2q without the fold
+    (32, 32, 32, 8, 128, [300 + 97 * i for i in range(10)], 0),
     # G*l_q = 160 > 128: mma.sync row blocks (64 + 64 + 32 rows) at d = 128
     (40, 40, 32, 8, 128, [2000], 0),
     # 19 x 8 = 152 (sequence, kv head) groups >= the SM count: the arrival-counter split
