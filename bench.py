@@ -576,7 +576,7 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak):
     from paper_2411_17116_b200 import ops
 
     out = []
-    for B, S in ((1, 32768), (1, 131072), (1, 1048576), (8, 131072), (32, 32768)):
+    for B, S in ((1, 16384), (1, 32768), (1, 131072), (1, 1048576), (8, 131072), (32, 32768)):
         page = 128
         pages = B * (S // page)
         kp = ops.prng_fill((pages, hkv, page, d), 21, 1, 1.0, torch.bfloat16, dev)

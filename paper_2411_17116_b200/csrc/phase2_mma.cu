@@ -711,27 +711,51 @@ namespace p2q {
 constexpr int BN = 128;                 // keys per tile
 constexpr int kSlab = 128 * 128;        // [128 rows x 64 bf16] SW128 slab
 constexpr int kTile = 2 * kSlab;        // [128 x 128] bf16
-constexpr int KST = 3, VST = 3;
+constexpr int KST = 2, VST = 3;
 constexpr int kQOff = 0;
 constexpr int kKOff = kQOff + kTile;
 constexpr int kVOff = kKOff + KST * kTile;
-constexpr int kBarOff = kVOff + VST * kTile;
+constexpr int kRedOff = kVOff + VST * kTile;      // [2 parity][2 half][128] f32 row maxima
+constexpr int kLOff = kRedOff + 2 * 2 * 128 * 4;  // [2 half][128] f32 partial row sums
+constexpr int kBarOff = kLOff + 2 * 128 * 4;
 constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 2 + 2 + 2;
 constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
-constexpr int kThreads = 192;           // warps 0-3 softmax (TMEM lanes), 4 TMA, 5 MMA
+// warps 0-7 softmax: warp w owns TMEM lanes 32*(w%4).. (rows) and S columns of half w/4;
+// warp 8 TMA, warp 9 MMA + TMEM allocation
+constexpr int kSoftmaxThreads = 256;
+constexpr int kThreads = kSoftmaxThreads + 64;
 constexpr int kOCol = 2 * BN;           // O after the two S buffers
 static_assert(kSmem <= 232448, "shared memory budget");
 }  // namespace p2q
 
-// P = hi + lo (both bf16) of 2^(s*sl2 - m) for one 128-column row: hi over S columns
-// [16c, 16c+16), lo over [64+16c, ...) for chunk c; returns the row sum of hi + lo.
+// One 64-column half of a row (columns colbase + [0, 64)): masked max of the raw scores.
 template <bool DIAG>
-__device__ __forceinline__ float exp_pack_hilo(const uint32_t (&sv)[4][32], uint32_t s_tm, int lim,
-                                               float sl2, float m) {
+__device__ __forceinline__ float row_max_half(const uint32_t (&sv)[2][32], int lim, int colbase) {
+  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float v0 = __uint_as_float(sv[c][e]), v1 = __uint_as_float(sv[c][e + 1]);
+      if (DIAG) {
+        if (colbase + c * 32 + e > lim) v0 = -INFINITY;
+        if (colbase + c * 32 + e + 1 > lim) v1 = -INFINITY;
+      }
+      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(v0, v1));
+    }
+  return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+}
+
+// P = hi + lo (both bf16) of 2^(s*sl2 - m) for one 64-column half row: hi packed over the
+// half's P columns at p_hi (16 columns per 32 keys), lo at p_lo; returns the sum of hi + lo.
+template <bool DIAG>
+__device__ __forceinline__ float exp_pack_hilo_half(const uint32_t (&sv)[2][32], uint32_t p_hi,
+                                                    uint32_t p_lo, int lim, int colbase, float sl2,
+                                                    float m) {
   float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < 2; ++c) {
     float p[32];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
@@ -745,7 +769,7 @@ __device__ __forceinline__ float exp_pack_hilo(const uint32_t (&sv)[4][32], uint
     for (int e = 0; e < 32; e += 2) {
       float p0 = p[e], p1 = p[e + 1];
       if (DIAG) {
-        const int col = c * 32 + e;
+        const int col = colbase + c * 32 + e;
         if (col > lim) p0 = 0.f;
         if (col + 1 > lim) p1 = 0.f;
       }
@@ -757,8 +781,8 @@ __device__ __forceinline__ float exp_pack_hilo(const uint32_t (&sv)[4][32], uint
       acc_bf16x2(acc.x, acc.y, wh);
       acc_bf16x2(acc.x, acc.y, wl);
     }
-    tmem_st16(s_tm + c * 16, hi);
-    tmem_st16(s_tm + 64 + c * 16, lo);
+    tmem_st16(p_hi + c * 16, hi);
+    tmem_st16(p_lo + c * 16, lo);
   }
   return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
 }
@@ -808,12 +832,12 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     mbar_init(q_full, 1);
     for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 8); }
     mbar_init(o_done, 1);
     mbar_init(o_last, 1);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc<512>(tmem_slot);
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -828,43 +852,62 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     return (int)(((int64_t)page * hkv + kvh) * page_size + row % page_size);
   };
 
-  if (warp == 4) {
-    if (lane == 0 && ntiles > 0) {
+  if (warp == 8) {
+    if (ntiles > 0) {
       // ================= TMA producer: Q once, then K (one tile ahead) and V =================
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      mbar_expect_tx(q_full, 2 * QR * 128);
-      for (int a = 0; a < 2; ++a)
-        tma_load_3d(smem + kQOff + a * kSlab, &tm_q, q_full, a * 64, kvh * G, b * lq);
+      // The whole warp resolves page-table entries 32 half-tiles at a time (lane l -> half
+      // w0 + l, one coalesced load); lane 0 issues the TMA loads.  K and V keep their own
+      // windows (V trails K), so no TMA waits behind a dependent table read.
+      if (lane == 0) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        mbar_expect_tx(q_full, 2 * QR * 128);
+        for (int a = 0; a < 2; ++a)
+          tma_load_3d(smem + kQOff + a * kSlab, &tm_q, q_full, a * 64, kvh * G, b * lq);
+      }
+      const int nhalves = 2 * ntiles;
+      auto half_row = [&](int h) -> int { return h < nhalves ? key_row(h >> 1, h & 1) : 0; };
+      int kw0 = 0, vw0 = 0;
+      int kcur = half_row(lane), vcur = kcur;
       int kt = 0, vt = 0;
       while (vt < ntiles) {
-        if (kt < ntiles && kt <= vt + 1) {
-          const int st = kt % KST;
-          if (kt >= KST) mbar_wait(&k_empty[st], ((kt / KST) + 1) & 1);
-          mbar_expect_tx(&k_full[st], kTile);
-          for (int hh = 0; hh < 2; ++hh) {
-            const int pr = key_row(kt, hh);
-            for (int a = 0; a < 2; ++a)
-              tma_load_2d(smem + kKOff + st * kTile + a * kSlab + hh * 64 * 128, &tm_k, &k_full[st],
-                          a * 64, pr);
+        const bool doK = kt < ntiles && kt <= vt + 1;
+        const int t = doK ? kt : vt;
+        int& w0 = doK ? kw0 : vw0;
+        int& cur = doK ? kcur : vcur;
+        if (2 * t + 1 >= w0 + 32) {  // slide this window (warp-uniform)
+          w0 = 2 * t;
+          cur = half_row(w0 + lane);
+        }
+        const int pr0 = __shfl_sync(0xffffffffu, cur, 2 * t - w0);
+        const int pr1 = __shfl_sync(0xffffffffu, cur, 2 * t + 1 - w0);
+        if (lane == 0) {
+          if (doK) {
+            const int st = kt % KST;
+            if (kt >= KST) mbar_wait(&k_empty[st], ((kt / KST) + 1) & 1);
+            mbar_expect_tx(&k_full[st], kTile);
+            unsigned char* dst = smem + kKOff + st * kTile;
+            for (int a = 0; a < 2; ++a) {
+              tma_load_2d(dst + a * kSlab, &tm_k, &k_full[st], a * 64, pr0);
+              tma_load_2d(dst + a * kSlab + 64 * 128, &tm_k, &k_full[st], a * 64, pr1);
+            }
+          } else {
+            const int st = vt % VST;
+            if (vt >= VST) mbar_wait(&v_empty[st], ((vt / VST) + 1) & 1);
+            mbar_expect_tx(&v_full[st], kTile);
+            unsigned char* dst = smem + kVOff + st * kTile;
+            for (int a = 0; a < 2; ++a) {
+              tma_load_2d(dst + a * kSlab, &tm_v, &v_full[st], a * 64, pr0);
+              tma_load_2d(dst + a * kSlab + 64 * 128, &tm_v, &v_full[st], a * 64, pr1);
+            }
           }
-          ++kt;
-          continue;
         }
-        const int st = vt % VST;
-        if (vt >= VST) mbar_wait(&v_empty[st], ((vt / VST) + 1) & 1);
-        mbar_expect_tx(&v_full[st], kTile);
-        for (int hh = 0; hh < 2; ++hh) {
-          const int pr = key_row(vt, hh);
-          for (int a = 0; a < 2; ++a)
-            tma_load_2d(smem + kVOff + st * kTile + a * kSlab + hh * 64 * 128, &tm_v, &v_full[st],
-                        a * 64, pr);
-        }
-        ++vt;
+        __syncwarp();
+        if (doK) ++kt; else ++vt;
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ================= MMA issuer =================
     // S(j) -> buffer j%2.  Order: S(0), S(1), then per tile j: P.V(j) (hi + lo halves of the
     // buffer), S(j+2) into the same buffer (in-order execution: P(j) is consumed first).
@@ -912,13 +955,18 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       }
     }
   } else {
-    // ================= softmax (warps 0-3: row r = TMEM lane) =================
-    const int r = warp * 32 + lane;
+    // ================= softmax: warps w and w+4 share the rows of TMEM lane quarter w%4,
+    // each on one 64-column half of every S row (two warps per SM sub-partition keep its
+    // MUFU pipe busy); the halves swap their row maxima through shared memory =================
+    const int hf = warp >> 2;                  // column half
+    const int r = (warp & 3) * 32 + lane;      // row = TMEM lane
     const int ti = r / G;  // token of this row (rows >= G*l_q are padding)
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    const uint32_t o_tm = tbase + lane_off + kOCol;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t o_tm = tbase + lane_off + kOCol + hf * 64;  // this half's O columns
+    float* red = reinterpret_cast<float*>(smem + kRedOff);   // [parity][half][row]
+    float* lsum = reinterpret_cast<float*>(smem + kLOff);    // [half][row]
     const float sl2 = scale_log2;
-    float m_run = -INFINITY, l_run = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;  // l_run: this half's share of the row sum
     // last visible key of this row relative to the split start (the split end and the row's
     // own-tail causal limit); padding rows (r >= G*l_q) take no mask at all — their values
     // only ever reach their own O lanes, which are discarded — so a warp with padding rows
@@ -931,10 +979,17 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       tc_fence_after();
       const int64_t base = r0 + (int64_t)j * BN;
       const int lim = max(-1, min(BN, last_rel - j * BN));  // columns c > lim are invisible
-      const bool masked = __any_sync(0xffffffffu, lim < BN - 1);
-      uint32_t sv[4][32];
-      tmem_ld_row128(s_tm, sv);
-      const float mx = (masked ? row_max_regs<true>(sv, lim) : row_max_regs<false>(sv, lim)) * sl2;
+      const bool masked = __any_sync(0xffffffffu, lim < hf * 64 + 63);
+      uint32_t sv[2][32];
+      tmem_ld32(s_tm + hf * 64, sv[0]);
+      tmem_ld32(s_tm + hf * 64 + 32, sv[1]);
+      tmem_wait_ld_tied(sv[0]);
+      tmem_wait_ld_tied(sv[1]);
+      const float mh = (masked ? row_max_half<true>(sv, lim, hf * 64)
+                               : row_max_half<false>(sv, lim, hf * 64)) * sl2;
+      red[((j & 1) * 2 + hf) * 128 + r] = mh;
+      named_barrier_sync(2, kSoftmaxThreads);
+      const float mx = fmaxf(mh, red[((j & 1) * 2 + (hf ^ 1)) * 128 + r]);
       float m_use = m_run, alpha = 1.f;
       const bool need = (j == 0) || (mx > m_run + 8.f);
       const bool warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
@@ -945,20 +1000,19 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       // rows with no visible key in this split (padding rows, or every key past the row's
       // own-tail limit): a finite m keeps their exp2 arguments finite
       if (pad || last_rel < 0) m_use = 0.f;
-      const float rs = masked ? exp_pack_hilo<true>(sv, s_tm, lim, sl2, m_use)
-                              : exp_pack_hilo<false>(sv, s_tm, lim, sl2, m_use);
+      // P of keys [64h, 64h+64): hi over columns [32h, 32h+32), lo over [64+32h, ...)
+      const uint32_t p_hi = s_tm + hf * 32, p_lo = s_tm + 64 + hf * 32;
+      const float rs = masked ? exp_pack_hilo_half<true>(sv, p_hi, p_lo, lim, hf * 64, sl2, m_use)
+                              : exp_pack_hilo_half<false>(sv, p_hi, p_lo, lim, hf * 64, sl2, m_use);
       if (r1 - base < BN) {
         // keys past the split end: their V rows may hold stale (even non-finite) data and
-        // P = 0 must not meet a NaN — zero them once the tile has landed
+        // P = 0 must not meet a NaN — zero them (half h clears V slab h) once the tile landed
         const int valid = (int)(r1 - base);
         mbar_wait(&v_full[j % VST], (j / VST) & 1);
         if (r >= valid) {
-          unsigned char* vrow = smem + kVOff + (j % VST) * kTile + r * 128;
+          uint4* vrow = reinterpret_cast<uint4*>(smem + kVOff + (j % VST) * kTile + hf * kSlab + r * 128);
 #pragma unroll
-          for (int a = 0; a < 2; ++a)
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              reinterpret_cast<uint4*>(vrow + a * kSlab)[c] = make_uint4(0, 0, 0, 0);
+          for (int c = 0; c < 8; ++c) vrow[c] = make_uint4(0, 0, 0, 0);
         }
         fence_proxy_async_smem();
       }
@@ -968,7 +1022,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         mbar_wait(o_done, (j - 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t orr[32];
           tmem_ld32(o_tm + c * 32, orr);
           tmem_wait_ld();
@@ -984,8 +1038,11 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j & 1]);
     }
-    // ---- epilogue: this split's partial of row r as {value, epoch} words; with one split
-    // (no fold) the final partial itself — local, or pushed to every rank's box ----
+    // ---- epilogue: this split's partial of row r (this half's 64 columns) as {value, epoch}
+    // words; with one split (no fold) the final partial itself — local, or pushed ----
+    lsum[hf * 128 + r] = l_run;
+    named_barrier_sync(2, kSoftmaxThreads);
+    const float l_row = l_run + lsum[(hf ^ 1) * 128 + r];
     const bool single = gridDim.x == 1;
     const uint32_t es = single ? 0u : next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y));
     const uint32_t ep = (single && pp.L.world > 0) ? exchange_epoch(pp) : 0u;
@@ -996,10 +1053,10 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     }
     const bool row_ok = r < QR;
     const int64_t orow = ((int64_t)b * lq + ti) * hq + kvh * G + r % G;
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    uint2* wo = w_out + (int64_t)split * part_rows * D + orow * D;
+    const float inv = l_row > 0.f ? 1.f / l_row : 0.f;
+    uint2* wo = w_out + (int64_t)split * part_rows * D + orow * D + hf * 64;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < 2; ++c) {
       uint32_t orr[32];
       if (ntiles > 0) {
         tmem_ld32(o_tm + c * 32, orr);
@@ -1014,14 +1071,14 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
           const float2 v2 =
               make_float2(__uint_as_float(orr[e]) * inv, __uint_as_float(orr[e + 1]) * inv);
           if (single)
-            put_out2(pp, ep, false, final_out, orow * D + c * 32 + e, v2);
+            put_out2(pp, ep, false, final_out, orow * D + hf * 64 + c * 32 + e, v2);
           else
             st_word2(wo + c * 32 + e, v2, es);
         }
       }
     }
-    if (row_ok) {
-      const float lv = l_run > 0.f ? (m_run + __log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+    if (row_ok && hf == 0) {
+      const float lv = l_row > 0.f ? (m_run + __log2f(l_row)) * 0.6931471805599453f : -INFINITY;
       if (single)
         put_lse(pp, ep, false, final_lse, orow, lv);
       else
@@ -1030,12 +1087,12 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 5) tmem_free<512>(tbase);
-  if (warp < 4 && gridDim.x > 1) {
+  if (warp == 9) tmem_free<512>(tbase);
+  if (warp < 8 && gridDim.x > 1) {
     // word-mode fold of the splits (+ the peer exchange push / merge when asked)
     const uint32_t es = next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y));
-    split_merge_words<D, 128>(b, kvh, 0, QR, lq, hq, G, w_out, w_lse, part_rows, es, final_out,
-                              final_lse, grp_epoch, pp);
+    split_merge_words<D, kSoftmaxThreads>(b, kvh, 0, QR, lq, hq, G, w_out, w_lse, part_rows, es,
+                                          final_out, final_lse, grp_epoch, pp);
   }
 }
 
