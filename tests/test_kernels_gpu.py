@@ -195,6 +195,9 @@ def test_kv_write_read_roundtrip(ops):
     (17, 0, 32, 8, 128, [4000], 5),
     (5, 5, 16, 4, 128, [700], 0),
     (32, 32, 32, 8, 128, [130], 2),
+    # K2q with G = 1 (no GQA: 40 tokens x 1 head per tile) and G = 8 (70B heads: 16 x 8)
+    (40, 40, 8, 8, 128, [1500], 0),
+    (16, 16, 64, 8, 128, [2500], 0),
     # batch 10 x 8 kv heads = 80 groups: one split each, K2q without the fold
     (32, 32, 32, 8, 128, [300 + 97 * i for i in range(10)], 0),
     # G*l_q = 160 > 128: mma.sync row blocks (64 + 64 + 32 rows) at d = 128
