@@ -718,13 +718,14 @@ constexpr int kVOff = kKOff + KST * kTile;
 constexpr int kRedOff = kVOff + VST * kTile;      // [2 parity][2 half][128] f32 row maxima
 constexpr int kLOff = kRedOff + 2 * 2 * 128 * 4;  // [2 half][128] f32 partial row sums
 constexpr int kBarOff = kLOff + 2 * 128 * 4;
-constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 2 + 2 + 2;
+constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 3 * 3 + 1;
 constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
 // warps 0-7 softmax: warp w owns TMEM lanes 32*(w%4).. (rows) and S columns of half w/4;
 // warp 8 TMA, warp 9 MMA + TMEM allocation
 constexpr int kSoftmaxThreads = 256;
 constexpr int kThreads = kSoftmaxThreads + 64;
-constexpr int kOCol = 2 * BN;           // O after the two S buffers
+constexpr int kSBuf = 3;                // S buffers in TMEM (3 x 128 + O 128 = 512 columns)
+constexpr int kOCol = kSBuf * BN;       // O after the S buffers
 static_assert(kSmem <= 232448, "shared memory budget");
 }  // namespace p2q
 
@@ -805,10 +806,10 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
   uint64_t* k_empty = k_full + KST;
   uint64_t* v_full = k_empty + KST;
   uint64_t* v_empty = v_full + VST;
-  uint64_t* s_full = v_empty + VST;  // [2]
-  uint64_t* p_full = s_full + 2;     // [2]
-  uint64_t* o_done = p_full + 2;     // every P.V (the rescale waits for the previous one)
-  uint64_t* o_last = o_done + 1;     // the last P.V (the epilogue)
+  uint64_t* s_full = v_empty + VST;  // [kSBuf]
+  uint64_t* p_full = s_full + kSBuf; // [kSBuf]
+  uint64_t* o_done = p_full + kSBuf; // [kSBuf]: P.V(j) -> o_done[j % kSBuf] (the rescale)
+  uint64_t* o_last = o_done + kSBuf; // the last P.V (the epilogue)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_last + 1);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
@@ -832,8 +833,8 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     mbar_init(q_full, 1);
     for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 8); }
-    mbar_init(o_done, 1);
+    for (int i = 0; i < kSBuf; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 8); }
+    for (int i = 0; i < kSBuf; ++i) mbar_init(&o_done[i], 1);
     mbar_init(o_last, 1);
     fence_mbar_init();
   }
@@ -872,7 +873,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       int kcur = half_row(lane), vcur = kcur;
       int kt = 0, vt = 0;
       while (vt < ntiles) {
-        const bool doK = kt < ntiles && kt <= vt + 1;
+        const bool doK = kt < ntiles && kt <= vt + kSBuf - 1;
         const int t = doK ? kt : vt;
         int& w0 = doK ? kw0 : vw0;
         int& cur = doK ? kcur : vcur;
@@ -926,20 +927,19 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
           const uint32_t off = (kk >> 2) * kSlab + (kk & 3) * 32;
           const uint64_t ad = umma_desc_sw128(q_addr + off, 16, 1024);
           const uint64_t bd = umma_desc_sw128(k_addr + st * kTile + off, 16, 1024);
-          umma_bf16_ss(tbase + (t & 1) * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+          umma_bf16_ss(tbase + (t % kSBuf) * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[t & 1]);
+        umma_commit(&s_full[t % kSBuf]);
         umma_commit(&k_empty[st]);
       };
       mbar_wait(q_full, 0);
-      issue_s(0);
-      if (ntiles > 1) issue_s(1);
+      for (int t = 0; t < kSBuf && t < ntiles; ++t) issue_s(t);
       for (int j = 0; j < ntiles; ++j) {
         const int vs = j % VST;
         mbar_wait(&v_full[vs], (j / VST) & 1);
-        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        mbar_wait(&p_full[j % kSBuf], (j / kSBuf) & 1);
         tc_fence_after();
-        const uint32_t pb = tbase + (j & 1) * BN;
+        const uint32_t pb = tbase + (j % kSBuf) * BN;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -948,10 +948,10 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
             umma_bf16_ts(tbase + kOCol, pb + h * 64 + kk * 8, bd, idesc_o,
                          (j > 0 || h > 0 || kk > 0) ? 1u : 0u);
           }
-        umma_commit(o_done);
+        umma_commit(&o_done[j % kSBuf]);
         if (j == ntiles - 1) umma_commit(o_last);
         umma_commit(&v_empty[vs]);
-        if (j + 2 < ntiles) issue_s(j + 2);
+        if (j + kSBuf < ntiles) issue_s(j + kSBuf);
       }
     }
   } else {
@@ -974,8 +974,8 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     const bool pad = r >= QR;
     const int last_rel = pad ? INT_MAX / 2 : (int)(min(r1 - 1, tail0 + ti) - r0);
     for (int j = 0; j < ntiles; ++j) {
-      const uint32_t s_tm = tbase + lane_off + (j & 1) * BN;
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      const uint32_t s_tm = tbase + lane_off + (j % kSBuf) * BN;
+      mbar_wait(&s_full[j % kSBuf], (j / kSBuf) & 1);
       tc_fence_after();
       const int64_t base = r0 + (int64_t)j * BN;
       const int lim = max(-1, min(BN, last_rel - j * BN));  // columns c > lim are invisible
@@ -1017,9 +1017,11 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         fence_proxy_async_smem();
       }
       if (warp_rescale) {
-        // O must hold P.V(j-1) before it is rescaled: wait for that commit (P.V(j) cannot
-        // have completed yet — it needs this tile's P — so the parity is unambiguous)
-        mbar_wait(o_done, (j - 1) & 1);
+        // O must hold P.V(j-1) before it is rescaled.  Its barrier o_done[(j-1) % kSBuf]
+        // completes once per kSBuf tiles: P.V(j-1-kSBuf) is done (S(j) was issued after
+        // P.V(j-kSBuf)) and P.V(j-1+kSBuf) cannot be (it needs a later P), so the parity of
+        // ((j-1) / kSBuf) is unambiguous
+        mbar_wait(&o_done[(j - 1) % kSBuf], ((j - 1) / kSBuf) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -1036,7 +1038,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       m_run = m_use;
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+      if (lane == 0) mbar_arrive(&p_full[j % kSBuf]);
     }
     // ---- epilogue: this split's partial of row r (this half's 64 columns) as {value, epoch}
     // words; with one split (no fold) the final partial itself — local, or pushed ----
