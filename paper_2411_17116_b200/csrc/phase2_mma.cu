@@ -100,7 +100,18 @@ __device__ __forceinline__ void k2_tr(int slot) {
   do {                    \
     if (cond) k2_tr(slot); \
   } while (0)
+// K2q timeline of CTA 0 (clock64): [tile][8] = softmax warp 0 lane 0: S seen, half max,
+// maxima swapped, exps + packs done, P handed over; MMA lane: P seen, P.V issued, next S issued
+__device__ long long g_k2q_trace[256][8];
+#define K2Q_TR(cond, t, slot)                                                   \
+  do {                                                                          \
+    if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < 256) \
+      g_k2q_trace[t][slot] = clock64();                                         \
+  } while (0)
 #else
+#define K2Q_TR(cond, t, slot) \
+  do {                        \
+  } while (0)
 #define K2_TR(cond, slot) \
   do {                    \
   } while (0)
@@ -711,7 +722,9 @@ namespace p2q {
 constexpr int BN = 128;                 // keys per tile
 constexpr int kSlab = 128 * 128;        // [128 rows x 64 bf16] SW128 slab
 constexpr int kTile = 2 * kSlab;        // [128 x 128] bf16
-constexpr int KST = 2, VST = 3;
+// K runs kSBuf tiles ahead of the softmax (QK^T of tile j+3 is issued right after P.V(j)),
+// so it gets the deeper ring; P.V(j)'s V tile is needed one period after P(j)
+constexpr int KST = 3, VST = 2;
 constexpr int kQOff = 0;
 constexpr int kKOff = kQOff + kTile;
 constexpr int kVOff = kKOff + KST * kTile;
@@ -873,7 +886,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       int kcur = half_row(lane), vcur = kcur;
       int kt = 0, vt = 0;
       while (vt < ntiles) {
-        const bool doK = kt < ntiles && kt <= vt + kSBuf - 1;
+        const bool doK = kt < ntiles && kt <= vt + kSBuf;
         const int t = doK ? kt : vt;
         int& w0 = doK ? kw0 : vw0;
         int& cur = doK ? kcur : vcur;
@@ -939,6 +952,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         mbar_wait(&v_full[vs], (j / VST) & 1);
         mbar_wait(&p_full[j % kSBuf], (j / kSBuf) & 1);
         tc_fence_after();
+        K2Q_TR(true, j, 5);
         const uint32_t pb = tbase + (j % kSBuf) * BN;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -948,10 +962,12 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
             umma_bf16_ts(tbase + kOCol, pb + h * 64 + kk * 8, bd, idesc_o,
                          (j > 0 || h > 0 || kk > 0) ? 1u : 0u);
           }
+        K2Q_TR(true, j, 6);
         umma_commit(&o_done[j % kSBuf]);
         if (j == ntiles - 1) umma_commit(o_last);
         umma_commit(&v_empty[vs]);
         if (j + kSBuf < ntiles) issue_s(j + kSBuf);
+        K2Q_TR(true, j, 7);
       }
     }
   } else {
@@ -977,6 +993,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       const uint32_t s_tm = tbase + lane_off + (j % kSBuf) * BN;
       mbar_wait(&s_full[j % kSBuf], (j / kSBuf) & 1);
       tc_fence_after();
+      K2Q_TR(threadIdx.x == 0, j, 0);
       const int64_t base = r0 + (int64_t)j * BN;
       const int lim = max(-1, min(BN, last_rel - j * BN));  // columns c > lim are invisible
       const bool masked = __any_sync(0xffffffffu, lim < hf * 64 + 63);
@@ -987,9 +1004,11 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       tmem_wait_ld_tied(sv[1]);
       const float mh = (masked ? row_max_half<true>(sv, lim, hf * 64)
                                : row_max_half<false>(sv, lim, hf * 64)) * sl2;
+      K2Q_TR(threadIdx.x == 0, j, 1);
       red[((j & 1) * 2 + hf) * 128 + r] = mh;
       named_barrier_sync(2, kSoftmaxThreads);
       const float mx = fmaxf(mh, red[((j & 1) * 2 + (hf ^ 1)) * 128 + r]);
+      K2Q_TR(threadIdx.x == 0, j, 2);
       float m_use = m_run, alpha = 1.f;
       const bool need = (j == 0) || (mx > m_run + 8.f);
       const bool warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
@@ -1004,6 +1023,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       const uint32_t p_hi = s_tm + hf * 32, p_lo = s_tm + 64 + hf * 32;
       const float rs = masked ? exp_pack_hilo_half<true>(sv, p_hi, p_lo, lim, hf * 64, sl2, m_use)
                               : exp_pack_hilo_half<false>(sv, p_hi, p_lo, lim, hf * 64, sl2, m_use);
+      K2Q_TR(threadIdx.x == 0, j, 3);
       if (r1 - base < BN) {
         // keys past the split end: their V rows may hold stale (even non-finite) data and
         // P = 0 must not meet a NaN — zero them (half h clears V slab h) once the tile landed
@@ -1038,6 +1058,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       m_run = m_use;
       tc_fence_before();
       __syncwarp();
+      K2Q_TR(threadIdx.x == 0, j, 4);
       if (lane == 0) mbar_arrive(&p_full[j % kSBuf]);
     }
     // ---- epilogue: this split's partial of row r (this half's 64 columns) as {value, epoch}
@@ -1262,6 +1283,11 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
 }
 
 #ifdef STAR_K1_TRACE
+int debug_k2q_trace(long long* host, int n) {
+  const int cap = 256 * 8;
+  if (n > cap) n = cap;
+  return cudaMemcpyFromSymbol(host, g_k2q_trace, n * sizeof(long long)) == cudaSuccess ? n : -4;
+}
 int debug_k2_trace(unsigned long long* host, int n) {
   const int cap = kK2TrCtas * 8;
   if (n > cap) n = cap;
@@ -1275,4 +1301,8 @@ int debug_k2_trace(unsigned long long* host, int n) {
 extern "C" int star_debug_k2_trace(unsigned long long* host, int n) {
   return star::debug_k2_trace(host, n);
 }
+#endif
+
+#ifdef STAR_K1_TRACE
+extern "C" int star_debug_k2q_trace(long long* host, int n) { return star::debug_k2q_trace(host, n); }
 #endif
