@@ -760,12 +760,13 @@ __device__ __forceinline__ float row_max_half(const uint32_t (&sv)[2][32], int l
   return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
 }
 
-// P = hi + lo (both bf16) of 2^(s*sl2 - m) for one 64-column half row: hi packed over the
-// half's P columns at p_hi (16 columns per 32 keys), lo at p_lo; returns the sum of hi + lo.
+// P = hi + lo (both bf16) of 2^(s*sl2 - m) for one 64-column half row.  Layout over the
+// half's own S columns: every 16 keys take 16 columns, hi (8 columns) then lo (8 columns),
+// so a 32-key chunk is ONE 32-column tcgen05.st; P.V reads hi of keys [16g, 16g+16) at
+// column 16g and lo at 16g + 8.  Returns the sum of hi + lo.
 template <bool DIAG>
-__device__ __forceinline__ float exp_pack_hilo_half(const uint32_t (&sv)[2][32], uint32_t p_hi,
-                                                    uint32_t p_lo, int lim, int colbase, float sl2,
-                                                    float m) {
+__device__ __forceinline__ float exp_pack_hilo_half(const uint32_t (&sv)[2][32], uint32_t p_base,
+                                                    int lim, int colbase, float sl2, float m) {
   float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
 #pragma unroll
@@ -778,7 +779,7 @@ __device__ __forceinline__ float exp_pack_hilo_half(const uint32_t (&sv)[2][32],
       p[e] = ex2v(x.x);
       p[e + 1] = ex2v(x.y);
     }
-    uint32_t hi[16], lo[16];
+    uint32_t w[32];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
       float p0 = p[e], p1 = p[e + 1];
@@ -789,14 +790,14 @@ __device__ __forceinline__ float exp_pack_hilo_half(const uint32_t (&sv)[2][32],
       }
       const uint32_t wh = pack_bf16x2v(p0, p1);
       const uint32_t wl = pack_bf16x2v(p0 - bf16lo(wh), p1 - bf16hi(wh));
-      hi[e >> 1] = wh;
-      lo[e >> 1] = wl;
+      const int g = e >> 4, k = (e & 15) >> 1;  // 16-key group in the chunk, pair in it
+      w[g * 16 + k] = wh;
+      w[g * 16 + 8 + k] = wl;
       float2& acc = rsum[(e >> 1) & 1];
       acc_bf16x2(acc.x, acc.y, wh);
       acc_bf16x2(acc.x, acc.y, wl);
     }
-    tmem_st16(p_hi + c * 16, hi);
-    tmem_st16(p_lo + c * 16, lo);
+    tmem_st32(p_base + c * 32, w);
   }
   return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
 }
@@ -955,13 +956,13 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         K2Q_TR(true, j, 5);
         const uint32_t pb = tbase + (j % kSBuf) * BN;
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t bd = umma_desc_sw128(v_addr + vs * kTile + kk * 16 * 128, kSlab, 1024);
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            const uint64_t bd = umma_desc_sw128(v_addr + vs * kTile + kk * 16 * 128, kSlab, 1024);
-            umma_bf16_ts(tbase + kOCol, pb + h * 64 + kk * 8, bd, idesc_o,
+          for (int h = 0; h < 2; ++h)  // hi at column 16kk, lo at 16kk + 8
+            umma_bf16_ts(tbase + kOCol, pb + kk * 16 + h * 8, bd, idesc_o,
                          (j > 0 || h > 0 || kk > 0) ? 1u : 0u);
-          }
+        }
         K2Q_TR(true, j, 6);
         umma_commit(&o_done[j % kSBuf]);
         if (j == ntiles - 1) umma_commit(o_last);
@@ -1019,10 +1020,10 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       // rows with no visible key in this split (padding rows, or every key past the row's
       // own-tail limit): a finite m keeps their exp2 arguments finite
       if (pad || last_rel < 0) m_use = 0.f;
-      // P of keys [64h, 64h+64): hi over columns [32h, 32h+32), lo over [64+32h, ...)
-      const uint32_t p_hi = s_tm + hf * 32, p_lo = s_tm + 64 + hf * 32;
-      const float rs = masked ? exp_pack_hilo_half<true>(sv, p_hi, p_lo, lim, hf * 64, sl2, m_use)
-                              : exp_pack_hilo_half<false>(sv, p_hi, p_lo, lim, hf * 64, sl2, m_use);
+      // P of keys [64h, 64h+64) over this half's own S columns [64h, 64h+64)
+      const uint32_t p_base = s_tm + hf * 64;
+      const float rs = masked ? exp_pack_hilo_half<true>(sv, p_base, lim, hf * 64, sl2, m_use)
+                              : exp_pack_hilo_half<false>(sv, p_base, lim, hf * 64, sl2, m_use);
       K2Q_TR(threadIdx.x == 0, j, 3);
       if (r1 - base < BN) {
         // keys past the split end: their V rows may hold stale (even non-finite) data and
