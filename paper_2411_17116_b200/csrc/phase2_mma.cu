@@ -926,7 +926,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     // ================= MMA issuer =================
     // S(j) -> buffer j%2.  Order: S(0), S(1), then per tile j: P.V(j) (hi + lo halves of the
     // buffer), S(j+2) into the same buffer (in-order execution: P(j) is consumed first).
-    if (lane == 0 && ntiles > 0) {
+    if (ntiles > 0) {  // the whole warp (converged): one elected lane issues each MMA
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, BN, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
       const uint32_t q_addr = smem_u32(smem + kQOff);
@@ -941,10 +941,10 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
           const uint32_t off = (kk >> 2) * kSlab + (kk & 3) * 32;
           const uint64_t ad = umma_desc_sw128(q_addr + off, 16, 1024);
           const uint64_t bd = umma_desc_sw128(k_addr + st * kTile + off, 16, 1024);
-          umma_bf16_ss(tbase + (t % kSBuf) * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+          umma_bf16_ss_warp(tbase + (t % kSBuf) * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[t % kSBuf]);
-        umma_commit(&k_empty[st]);
+        umma_commit_warp(&s_full[t % kSBuf]);
+        umma_commit_warp(&k_empty[st]);
       };
       mbar_wait(q_full, 0);
       for (int t = 0; t < kSBuf && t < ntiles; ++t) issue_s(t);
@@ -960,13 +960,13 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
           const uint64_t bd = umma_desc_sw128(v_addr + vs * kTile + kk * 16 * 128, kSlab, 1024);
 #pragma unroll
           for (int h = 0; h < 2; ++h)  // hi at column 16kk, lo at 16kk + 8
-            umma_bf16_ts(tbase + kOCol, pb + kk * 16 + h * 8, bd, idesc_o,
+            umma_bf16_ts_warp(tbase + kOCol, pb + kk * 16 + h * 8, bd, idesc_o,
                          (j > 0 || h > 0 || kk > 0) ? 1u : 0u);
         }
         K2Q_TR(true, j, 6);
-        umma_commit(&o_done[j % kSBuf]);
-        if (j == ntiles - 1) umma_commit(o_last);
-        umma_commit(&v_empty[vs]);
+        umma_commit_warp(&o_done[j % kSBuf]);
+        if (j == ntiles - 1) umma_commit_warp(o_last);
+        umma_commit_warp(&v_empty[vs]);
         if (j + kSBuf < ntiles) issue_s(j + kSBuf);
         K2Q_TR(true, j, 7);
       }
