@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
-    if (lane == 0) {
+    {  // the whole warp, converged: one elected lane issues each MMA / commit
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, C::BN, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
       const uint32_t q_addr = smem_u32(smem + C::kQOff);
@@ -194,15 +194,15 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
           const uint32_t off = (kk >> 2) * C::kSlab + (kk & 3) * 32;
           const uint64_t ad = umma_desc_sw128(q_addr + i * C::kTile + off, 16, 1024);
           const uint64_t bd = umma_desc_sw128(k_addr + st * C::kTile + off, 16, 1024);
-          umma_bf16_ss(tbase + i * C::BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+          umma_bf16_ss_warp(tbase + i * C::BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[i]);
+        umma_commit_warp(&s_full[i]);
       };
       mbar_wait(q_full, 0);
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
       for (int i = 0; i < NQ; ++i) issue_s(i, 0);
-      umma_commit(&k_empty[0]);
+      umma_commit_warp(&k_empty[0]);
       for (int j = 0; j < nkv; ++j) {
         const int vs = j % C::VST;
         mbar_wait(&v_full[vs], (j / C::VST) & 1);
@@ -217,15 +217,15 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
           for (int kk = 0; kk < C::BN / 16; ++kk) {
             const uint64_t bd = umma_desc_sw128(v_addr + vs * C::kTile + kk * 16 * 128, C::kSlab,
                                                 1024);
-            umma_bf16_ts(tbase + NQ * C::BN + i * D, tbase + i * C::BN + kk * 8, bd, idesc_o,
+            umma_bf16_ts_warp(tbase + NQ * C::BN + i * D, tbase + i * C::BN + kk * 8, bd, idesc_o,
                          (j > 0 || kk > 0) ? 1u : 0u);
           }
-          umma_commit(&o_done[i]);
+          umma_commit_warp(&o_done[i]);
           if (next) issue_s(i, ks);
           K1_TR(bx == 0 && j < 256, 2 * 256 * 5 + (j * 2 + i) * 2 + 1);
         }
-        umma_commit(&v_empty[vs]);
-        if (next) umma_commit(&k_empty[ks]);
+        umma_commit_warp(&v_empty[vs]);
+        if (next) umma_commit_warp(&k_empty[ks]);
       }
     }
   } else {
