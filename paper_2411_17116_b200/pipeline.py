@@ -48,6 +48,17 @@ class LayerEncodePlan:
     ctx_rows: int = 0
     h2d: list = field(default_factory=list)
     d2d: list = field(default_factory=list)
+    # cross-call ordering of back-to-back encodes (wait=False): per segment, the previous
+    # call's last compute (it read the staging rows the next H2D overwrites) and last D2H
+    # (it read the output rows the next K1 overwrites); `done` = the last call finished
+    comp_done: list = field(default_factory=list)
+    d2h_done: list = field(default_factory=list)
+    done: object = None
+
+    def synchronize(self) -> None:
+        """Block the host until the last encode (including its D2H) has finished."""
+        if self.done is not None:
+            self.done.synchronize()
 
     @classmethod
     def create(cls, seg: Sequence[int], own: Sequence[int], hq: int, hkv: int, d: int,
@@ -144,24 +155,36 @@ def _clip(ranges, lo: int, hi: int):
 
 
 def _encode(plan: LayerEncodePlan, copy_in, positions, k_pages, v_pages, page_table, out_host,
-            theta):
-    """Per segment and query-row part: H2D (copy_in) | RoPE + KV write + K1 range | D2H."""
+            theta, wait: bool = True):
+    """Per segment and query-row part: H2D (copy_in) | RoPE + KV write + K1 range | D2H.
+
+    wait=False returns without making the current stream wait for the pipeline, so the next
+    call's H2D (fill) overlaps this call's last D2H (drain) and compute; cross-call hazards on
+    the staging and output rows are ordered per segment by events (plan.comp_done / d2h_done).
+    The caller then waits on plan.done (an event) or calls plan.synchronize()."""
     s_in, s_comp, s_out = plan.streams
     cur = torch.cuda.current_stream(plan.q.device)
-    s_in.wait_stream(cur)
-    s_comp.wait_stream(cur)
-    s_out.wait_stream(cur)
+    start = torch.cuda.Event()
+    start.record(cur)
+    for st in (s_in, s_comp, s_out):
+        st.wait_event(start)
     n = len(plan.seg) - 1
+    if len(plan.comp_done) != n:
+        plan.comp_done, plan.d2h_done = [None] * n, [None] * n
     for i in range(n):
         a, b = plan.seg[i], plan.seg[i + 1]
         cuts = _cuts(b - a, i == 0, i == n - 1)
-        for p0, p1 in zip(cuts[:-1], cuts[1:]):
+        for k_part, (p0, p1) in enumerate(zip(cuts[:-1], cuts[1:])):
             with torch.cuda.stream(s_in):
+                if k_part == 0 and plan.comp_done[i] is not None:
+                    s_in.wait_event(plan.comp_done[i])
                 copy_in(i, a + p0, a + p1)
             ev_in = torch.cuda.Event()
             ev_in.record(s_in)
             with torch.cuda.stream(s_comp):
                 s_comp.wait_event(ev_in)
+                if k_part == 0 and plan.d2h_done[i] is not None:
+                    s_comp.wait_event(plan.d2h_done[i])
                 r0, r1 = a + p0, a + p1
                 ops.rope_qkv(plan.q[r0:r1], plan.k[r0:r1], plan.v[r0:r1], positions[r0:r1], theta,
                              q_out=plan.q_rot[r0:r1], k_out=plan.k_rot[r0:r1],
@@ -175,16 +198,23 @@ def _encode(plan: LayerEncodePlan, copy_in, positions, k_pages, v_pages, page_ta
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_c)
                 out_host[a + p0:a + p1].copy_(plan.out[a + p0:a + p1], non_blocking=True)
-    cur.wait_stream(s_out)
-    cur.wait_stream(s_comp)
+        plan.comp_done[i] = ev_c
+        ev_o = torch.cuda.Event()
+        ev_o.record(s_out)
+        plan.d2h_done[i] = ev_o
+    s_out.wait_stream(s_comp)
+    plan.done = torch.cuda.Event()
+    plan.done.record(s_out)
+    if wait:
+        cur.wait_event(plan.done)
 
 
 def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch.Tensor,
                       v_host: torch.Tensor, positions: torch.Tensor, k_pages: torch.Tensor,
                       v_pages: torch.Tensor, page_table: torch.Tensor, out_host: torch.Tensor,
-                      theta: float = 10000.0) -> None:
+                      theta: float = 10000.0, wait: bool = True) -> None:
     """Phase-1 encode of one layer from pinned host q/k/v (pre-RoPE, augmented layout) to
-    pinned host out.
+    pinned host out (wait: see _encode).
 
     positions: device int64 [rows].  Returns when every copy and kernel is queued; the
     caller synchronises (or records an event) on the current stream, which is made to wait
@@ -195,13 +225,14 @@ def encode_layer_host(plan: LayerEncodePlan, q_host: torch.Tensor, k_host: torch
         plan.k[r0:r1].copy_(k_host[r0:r1], non_blocking=True)
         plan.v[r0:r1].copy_(v_host[r0:r1], non_blocking=True)
 
-    _encode(plan, copy_in, positions, k_pages, v_pages, page_table, out_host, theta)
+    _encode(plan, copy_in, positions, k_pages, v_pages, page_table, out_host, theta, wait)
 
 
 def encode_layer_host_context(plan: LayerEncodePlan, q_ctx: torch.Tensor, k_ctx: torch.Tensor,
                               v_ctx: torch.Tensor, positions: torch.Tensor, k_pages: torch.Tensor,
                               v_pages: torch.Tensor, page_table: torch.Tensor,
-                              out_host: torch.Tensor, theta: float = 10000.0) -> None:
+                              out_host: torch.Tensor, theta: float = 10000.0,
+                              wait: bool = True) -> None:
     """As encode_layer_host, from pinned host q/k/v in the context layout (each distinct
     context row once, plan.set_context_layout): rows of a block cross PCIe once, anchor
     rows are replicated from the device copy of block 0.  out_host is the full augmented
@@ -221,4 +252,4 @@ def encode_layer_host_context(plan: LayerEncodePlan, q_ctx: torch.Tensor, k_ctx:
             plan.k[r0:r0 + m].copy_(plan.k[src:src + m], non_blocking=True)
             plan.v[r0:r0 + m].copy_(plan.v[src:src + m], non_blocking=True)
 
-    _encode(plan, copy_in, positions, k_pages, v_pages, page_table, out_host, theta)
+    _encode(plan, copy_in, positions, k_pages, v_pages, page_table, out_host, theta, wait)

@@ -75,3 +75,44 @@ def test_host_pipeline_layouts_match_device_path(G, rank):
     torch.cuda.synchronize()
     assert torch.equal(out_c.to(dev), ref)
     assert torch.equal(kp2, kp0) and torch.equal(vp2, vp0)
+
+
+def test_back_to_back_encodes_without_waiting():
+    """Two encodes of different inputs queued back to back with wait=False (the next fill
+    overlaps the previous drain): each output equals its own device-path reference."""
+    from paper_2411_17116_b200 import ops, pipeline
+
+    dev = torch.device("cuda", 0)
+    L, b, a, hq, hkv, d = 1024, 256, 256, 8, 2, 128
+    n = L // b
+    pos, seg, own = [], [0], []
+    for i in range(n):
+        rows = list(range(a)) + list(range(i * b, i * b + b)) if i else list(range(b))
+        pos += rows
+        seg.append(seg[-1] + len(rows))
+        own.append(b)
+    R = seg[-1]
+    positions = torch.tensor(pos, dtype=torch.int64, device=dev)
+    page = 128
+    n_pages = -(-sum(own) // page) + 1
+    table = torch.arange(n_pages, dtype=torch.int32, device=dev)
+    kp = torch.zeros((n_pages, hkv, page, d), dtype=torch.bfloat16, device=dev)
+    vp = torch.zeros_like(kp)
+    plan = pipeline.LayerEncodePlan.create(seg, own, hq, hkv, d, dev)
+    refs, outs, hosts = [], [], []
+    for seed in (11, 23):
+        q, k, v = (ops.prng_fill((L, h, d), seed + s_, 1, 1.0, torch.bfloat16, dev)
+                   .index_select(0, positions).contiguous() for s_, h in ((1, hq), (2, hkv), (3, hkv)))
+        q_rot, k_rot = torch.empty_like(q), torch.empty_like(k)
+        ops.rope(q, positions, 10000.0, out=q_rot)
+        ops.rope(k, positions, 10000.0, out=k_rot)
+        refs.append(ops.phase1_fwd(q_rot, k_rot, v, seg)[0])
+        hosts.append(tuple(t.cpu().pin_memory() for t in (q, k, v)))
+        outs.append(torch.empty((R, hq, d), dtype=torch.bfloat16, pin_memory=True))
+    torch.cuda.synchronize()
+    for (hq_, hk_, hv_), out_h in zip(hosts, outs):
+        pipeline.encode_layer_host(plan, hq_, hk_, hv_, positions, kp, vp, table, out_h,
+                                   wait=False)
+    plan.synchronize()
+    for ref, out_h in zip(refs, outs):
+        assert torch.equal(out_h.to(dev), ref)
