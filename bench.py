@@ -445,8 +445,12 @@ def run_ours(args):
     packed, po, pl = ops.packed_partial(hq, d, dev)
     gathered = torch.empty(world * hq * (d + 1), dtype=torch.float32, device=dev)
     ws = ops.Phase2Workspace()
+    peer_note = None
     if world > 1:
-        ex = D.open_peer_exchange(hq, hkv, d, dev)
+        try:
+            ex = D.open_peer_exchange(hq, hkv, d, dev)
+        except D.PeerExchangeUnavailable as exc:  # same outcome on every rank
+            ex, peer_note = None, f"peer exchange unavailable ({exc}); all-gather transport"
     else:
         ex = D.local_peer_exchanges(1, hq, hkv, d, dev)[0]
 
@@ -463,7 +467,7 @@ def run_ours(args):
         dist.all_gather_into_tensor(gathered, packed)
         return ops.merge_packed(gathered.view(world, -1), hq, d)
 
-    decode_step = peer_step if world > 1 else k2_only
+    decode_step = (peer_step if ex is not None else collective_step) if world > 1 else k2_only
 
     def capture(fn, reps=1):
         """CUDA graph of `reps` calls of fn (a decode loop replays a fixed graph per token)."""
@@ -500,7 +504,7 @@ def run_ours(args):
     n_k2 = 20
     k2_graph = capture(lambda: ops.phase2_partial(qd, kpool, vpool, table.view(1, -1), kv_len,
                                                   own_rows, workspace=ws), n_k2)
-    exch_us = time_replays(capture(peer_step), 200)
+    exch_us = time_replays(capture(peer_step), 200) if ex is not None else peer_note
     coll_us = None
     if world > 1 and backend != "nccl":
         coll_us = f"unmeasured ({backend} collectives cannot be graph-captured)"
@@ -530,9 +534,9 @@ def run_ours(args):
                      "frac": kv_bytes / (k2_us * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6532.9),
                      "bytes_per_launch": kv_bytes,
                      "note": "K2 split-KV partial + in-GPU split merge; bytes = local KV rows x 8 heads x 128 x 2 (K,V) x 2 B"},
-        "exchange": ("fused peer exchange, one kernel per token-layer: K2 stores its partial "
-                     "into every rank's box over NVLink peer memory and merges every rank's "
-                     "partial as the words land (no NCCL)") if world > 1
+        "exchange": (peer_note or "fused peer exchange, one kernel per token-layer: K2 stores "
+                     "its partial into every rank's box over NVLink peer memory and merges "
+                     "every rank's partial as the words land (no NCCL)") if world > 1
                     else "none (1 rank: the K2 partial is the answer)",
         "peer_exchange_us": exch_us,
         "peer_exchange_note": ("star_phase2_exchange per token" if world > 1 else

@@ -197,25 +197,49 @@ def _alloc_box(world, cap_rows, cap_groups, d, device) -> torch.Tensor:
     return torch.zeros(n, dtype=torch.uint8, device=device)
 
 
+class PeerExchangeUnavailable(RuntimeError):
+    """Raised on EVERY rank when any rank cannot map the exchange boxes (no CUDA IPC, e.g.
+    virtual-memory allocations or ranks without peer access); callers fall back to the
+    all-gather transport."""
+
+
 def open_peer_exchange(cap_rows: int, cap_groups: int, d: int, device, group=None) -> PeerExchange:
     """Collective: allocate this rank's box, swap CUDA-IPC handles with every rank (one
-    all_gather_object over `group`, any backend) and map the peers' boxes."""
+    all_gather_object over `group`, any backend) and map the peers' boxes.  Every rank gets
+    the same outcome: a PeerExchange, or PeerExchangeUnavailable."""
     from . import ops
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     box = _alloc_box(world, cap_rows, cap_groups, d, device)
     torch.cuda.synchronize(device)  # the zeroed box is visible before any peer can write it
-    handle, off = ops.ipc_get_handle(box)
+    try:
+        handle, off = ops.ipc_get_handle(box)
+        mine = (True, handle, off, "")
+    except Exception as exc:  # noqa: BLE001 - reported collectively below
+        mine = (False, b"", 0, f"rank {rank}: {exc}")
     allh = [None] * world
-    dist.all_gather_object(allh, (handle, off), group=group)
-    boxes, opened = [], []
-    for r, (h, o) in enumerate(allh):
+    dist.all_gather_object(allh, mine, group=group)
+    bad = [m[3] for m in allh if not m[0]]
+    if bad:
+        raise PeerExchangeUnavailable("; ".join(bad))
+    boxes, opened, err = [], [], ""
+    for r, (_, h, o, _) in enumerate(allh):
         if r == rank:
             boxes.append(box.data_ptr())
-        else:
+            continue
+        try:
             ptr = ops.ipc_open_handle(h, o)
-            boxes.append(ptr)
-            opened.append((ptr, o))
+        except Exception as exc:  # noqa: BLE001
+            err = f"rank {rank} mapping rank {r}: {exc}"
+            break
+        boxes.append(ptr)
+        opened.append((ptr, o))
+    status = [None] * world
+    dist.all_gather_object(status, err, group=group)
+    if any(status):
+        for ptr, o in opened:
+            ops.ipc_close_handle(ptr, o)
+        raise PeerExchangeUnavailable("; ".join(x for x in status if x))
     dist.barrier(group=group)  # every box mapped everywhere before the first exchange
     return PeerExchange(rank, boxes, cap_rows, cap_groups, d, box, opened)
 
@@ -348,7 +372,8 @@ def start_session_dist(weights, tokens, plan: BlockPlan, spec: AnchorSpec, prng=
     backend, "auto" = peer when the group runs NCCL (one GPU per rank), else collective."""
     if transport not in ("auto", "peer", "collective"):
         raise ConfigError(f"unknown phase-2 transport {transport!r}")
-    if transport == "auto":
+    auto = transport == "auto"
+    if auto:
         transport = "peer" if dist.get_backend(group) == "nccl" else "collective"
     world = dist.get_world_size(group)
     L = plan.context_len
@@ -362,8 +387,13 @@ def start_session_dist(weights, tokens, plan: BlockPlan, spec: AnchorSpec, prng=
     if transport == "peer":
         cfg = weights.config
         # capacity: the query encode's l_q rows x heads (decode steps use a prefix of it)
-        sess.exchange = open_peer_exchange(len(query) * cfg.heads, pool.k[0].shape[1],
-                                           cfg.head_dim, weights.embedding.device, group)
+        try:
+            sess.exchange = open_peer_exchange(len(query) * cfg.heads, pool.k[0].shape[1],
+                                               cfg.head_dim, weights.embedding.device, group)
+        except PeerExchangeUnavailable:
+            if not auto:
+                raise
+            sess.exchange = None  # every rank falls back to the all-gather transport
     if dist.get_rank(group) == q_rank:
         sess.ledger += [(2, q_rank, r, "query_broadcast", len(query)) for r in range(world)
                         if r != q_rank]
