@@ -129,3 +129,56 @@ def test_phase2_ledger_matches_golden_csv():
         rows += D.phase2_ledger_rows(qh, hosts, layers, H, 1, hd)
     csv = "phase,src,dst,kind,scalar_count\n" + "".join(f"{a},{b},{c},{k},{n}\n" for a, b, c, k, n in rows)
     assert csv == str(g["ledger_csv"])
+
+
+def _fallback_worker(rank, world, port, failing, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_17116_b200 import dist as D
+        from paper_2411_17116_b200 import ops
+
+        # host-only stand-ins: no device here, so the box is a CPU tensor, the IPC export
+        # fails on the `failing` rank and "maps" (returns a fake address) elsewhere
+        torch.cuda.synchronize = lambda *a, **k: None
+
+        def get_handle(t):
+            if rank == failing:
+                raise RuntimeError("no CUDA IPC for this allocation")
+            return b"\0" * 64, 0
+
+        ops.ipc_get_handle = get_handle
+        ops.ipc_open_handle = lambda h, o: 0x1000
+        ops.ipc_close_handle = lambda p, o: None
+        try:
+            D.open_peer_exchange(8, 2, 64, "cpu")
+            q.put((rank, "opened"))
+        except D.PeerExchangeUnavailable as exc:
+            q.put((rank, f"unavailable: {exc}"))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, f"error: {exc!r}"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("failing", [-1, 1])
+def test_peer_exchange_setup_outcome_is_collective(failing):
+    """open_peer_exchange: one rank unable to export its box makes EVERY rank raise
+    PeerExchangeUnavailable (the status is all-gathered), so the transport=auto fallback is
+    taken together; with no failure every rank opens."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fallback_worker, args=(r, 2, port, failing, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    if failing < 0:
+        assert out == {0: "opened", 1: "opened"}, out
+    else:
+        assert all(v.startswith("unavailable") and "rank 1" in v for v in out.values()), out
