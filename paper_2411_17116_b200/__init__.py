@@ -12,11 +12,12 @@ from .attention import (AttnScale, PartialAttention, causal_attention, merge_par
 from .baselines import (DivergenceReport, FlopReport, divergence, global_pairs, ring_model,
                         star_model)
 from .blocking import (CONTENT_MODES, POSITION_MODES, AnchorSpec, AugmentedBlock, BlockPlan,
-                       KVCache, PagedKVPool, augment, partition, sparsity_pattern)
+                       KVCache, PagedKVPool, augment, encode_block, partition, sparsity_pattern)
 from .errors import ConfigError, DeviceError, DomainError, ShapeError, StarSimError
 from .model import (ModelConfig, ModelWeights, embed, forward_global, greedy_decode_global,
                     init_model, layer_step, logits_from)
-from .numerics import Prng, RopeConfig, default_dtype, precision, prng_fill, set_default_dtype
+from .numerics import (Prng, RopeConfig, default_dtype, precision, prng_fill, rope_apply,
+                       set_default_dtype)
 from .sim import (CommLedger, DecodeSession, Host, LedgerEntry, decode, forward_star,
                   run_phase1, run_phase2_step, set_query_host, start_session)
 

@@ -205,6 +205,10 @@ class PagedKVPool:
         self.positions: list[int] = []
         self.k = self.v = None
         self.page_table = None
+        # device mirror of layer_rows: the K2 kv_len argument and the row counter of
+        # append_rope (graph-safe: a captured decode step advances it on the device)
+        self.kv_len_dev = torch.zeros(layers, dtype=torch.int32, device=self.device)
+        self._workspace = None
         self._alloc(max(capacity_rows, page_size))
 
     def _alloc(self, rows: int) -> None:
@@ -223,9 +227,18 @@ class PagedKVPool:
     def capacity(self) -> int:
         return self.k.shape[1] * self.page_size
 
-    def reserve(self, rows: int) -> None:
+    def reserve(self, rows: int, exact: bool = False) -> None:
+        """Grow to at least `rows` rows (doubling, or exactly `rows` rounded to pages)."""
         if rows > self.capacity:
-            self._alloc(max(rows, 2 * self.capacity))
+            self._alloc(rows if exact else max(rows, 2 * self.capacity))
+
+    @property
+    def workspace(self):
+        """This pool's K2 split workspace (one per pool, so the hosts' launches never share
+        split counters and each keeps a stable shape signature)."""
+        if self._workspace is None:
+            self._workspace = ops.Phase2Workspace()
+        return self._workspace
 
     def write(self, layer: int, k: torch.Tensor, v: torch.Tensor, row0: int) -> None:
         """Write k/v [n, hkv, d] at logical rows [row0, row0+n) of `layer`."""
@@ -233,7 +246,9 @@ class PagedKVPool:
         self.reserve(row0 + n)
         ops.kv_write(k.to(self.dtype), v.to(self.dtype), self.k[layer], self.v[layer],
                      self.page_table, row0)
-        self.layer_rows[layer] = max(self.layer_rows[layer], row0 + n)
+        if row0 + n > self.layer_rows[layer]:
+            self.layer_rows[layer] = row0 + n
+            self.kv_len_dev[layer:layer + 1].fill_(row0 + n)  # stream-ordered, no host copy
 
     def append(self, layer: int, k: torch.Tensor, v: torch.Tensor, positions) -> None:
         """Append rows to one layer (new positions are recorded by the first layer to reach them)."""
@@ -245,11 +260,29 @@ class PagedKVPool:
         if row0 + len(pos) > len(self.positions):
             self.positions.extend(pos[len(self.positions) - row0:])
 
+    def append_rope(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                    positions: torch.Tensor, theta: float) -> torch.Tensor:
+        """Graph-safe append of one step's rows (the fused prologue): RoPE of q
+        and k at the device `positions`, rotated k and raw v written at the rows the device
+        counter kv_len_dev[layer] names, counter advanced on the device.  Returns rotated q.
+        The host mirror (layer_rows, positions) is the caller's to advance (DeviceDecoder)."""
+        n = k.shape[0]
+        rows = self.kv_len_dev[layer:layer + 1].to(torch.int64)
+        if n > 1:
+            rows = rows + torch.arange(n, dtype=torch.int64, device=self.device)
+        dt = self.dtype
+        qo, _ = ops.rope_qkv(q.to(dt).contiguous(), k.to(dt).contiguous(), v.to(dt).contiguous(),
+                             positions, theta, cache_rows=rows, k_pages=self.k[layer],
+                             v_pages=self.v[layer], page_table=self.page_table)
+        self.kv_len_dev[layer:layer + 1] += n
+        return qo
+
     def rows(self, layer: int) -> int:
         return self.layer_rows[layer]
 
     def kv_len_tensor(self, layer: int) -> torch.Tensor:
-        return torch.tensor([self.layer_rows[layer]], dtype=torch.int32, device=self.device)
+        """[1] int32 device view of layer's row count (no host->device copy per call)."""
+        return self.kv_len_dev[layer:layer + 1]
 
     def dense(self, layer: int, head: int | None = None):
         """Materialise a layer's rows densely: ([rows, hkv, d], [rows, hkv, d]) (checks only)."""
@@ -264,12 +297,15 @@ class KVCache:
 
     Construct either from dense keys/values (like the reference) — which
     creates a private one-layer, one-head pool — or as a view onto a host pool.
-    `append` grows the pool in place and returns self.
+    `append` on a dense-constructed cache returns a NEW cache and leaves this one unchanged
+    (the reference's value semantics, ss/blocking.py:161-170); on a host-pool view it grows
+    the host's pool in place and returns self (the protocol's query-host append).
     """
 
     def __init__(self, keys=None, values=None, positions=(), host: int = 0, *,
                  pool: PagedKVPool | None = None, layer: int = 0, head: int = 0):
         self.host = host
+        self._private = pool is None
         if pool is None:
             k = _as_device_2d(keys)
             vv = _as_device_2d(values)
@@ -307,6 +343,12 @@ class KVCache:
         pos = tuple(positions)
         if k.shape[0] != v.shape[0] or k.shape[0] != len(pos):
             raise ShapeError("appended keys/values/positions disagree in length")
+        if self._private:
+            if self.rows and k.shape[1] != self.pool.head_dim:
+                raise ShapeError("appended keys must share head_dim")
+            keys = torch.cat([self.keys, k]) if self.rows else k
+            values = torch.cat([self.values, v]) if self.rows else v
+            return KVCache(keys, values, self.positions + tuple(int(p) for p in pos), self.host)
         if self.pool.hkv != 1:
             raise ShapeError("append through a multi-head pool goes through PagedKVPool.append")
         self.pool.append(self.layer, k.unsqueeze(1), v.unsqueeze(1), pos)
@@ -329,3 +371,29 @@ def _as_device_2d(x) -> torch.Tensor:
     if not t.is_cuda:
         t = t.cuda()
     return t.to(default_dtype())
+
+
+def encode_block(block: AugmentedBlock, embedding, wq, wk, wv, rope, host: int = 0) -> KVCache:
+    """One attention channel over an augmented block, keeping only the own rows' K/V
+    (ss/blocking.py:239-265).  The whole block (anchor rows included) runs as queries
+    through the causal block encode (K1 in bf16, the fp32 check-mode kernel otherwise); the
+    outputs are computed and dropped as in the reference.  Returns KVCache(rotated k[a:],
+    v[a:], own positions, host)."""
+    from .attention import causal_attention
+    from .errors import DomainError
+    from .numerics import rope_apply
+
+    emb = _as_device_2d(embedding).float()
+    for t in block.token_ids:
+        if not 0 <= t < emb.shape[0]:
+            raise DomainError(f"token id {t} outside embedding table of {emb.shape[0]}")
+    idx = torch.tensor(block.token_ids, dtype=torch.long, device=emb.device)
+    x = emb.index_select(0, idx)
+    dt = default_dtype()
+    proj = [(x @ _as_device_2d(w).float()).to(dt) for w in (wq, wk, wv)]
+    q = rope_apply(proj[0], block.position_ids, rope)
+    k = rope_apply(proj[1], block.position_ids, rope)
+    v = proj[2]
+    causal_attention(q, k, v)  # anchor-row outputs are computed, then dropped
+    lo = block.anchor_prefix_len
+    return KVCache(k[lo:], v[lo:], block.own_positions, host)

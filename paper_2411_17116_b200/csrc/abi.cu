@@ -2,6 +2,7 @@
 // mirror the reference's ShapeError / DomainError / ConfigError conditions,
 // then dispatch to the sm_100a kernels.
 #include <stdarg.h>
+#include <algorithm>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -53,19 +54,6 @@ int attention_simt(const void*, const void*, const void*, int, SegTable&, int, i
                    int64_t, int, void*, int, int64_t, float*, int64_t, cudaStream_t);
 int phase1_tc(const void*, const void*, const void*, SegTable&, int, int, int, int64_t, int64_t,
               int64_t, void*, int, int64_t, float*, int64_t, cudaStream_t);
-int phase1_tc64(const void*, const void*, const void*, SegTable&, int, int, int64_t, int64_t,
-                int64_t, void*, int, int64_t, float*, int64_t, cudaStream_t);
-
-// K1 variant: "s128" (128-key tiles, default) or "db64" (64-key tiles, double-buffered S/P
-// in TMEM; correct, measured 7% slower on cfg2 — kept for tuning via STAR_K1_VARIANT=db64).
-static bool use_db64() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("STAR_K1_VARIANT");
-    v = (e != nullptr && e[0] == 'd') ? 1 : 0;  // default: s128 (measured faster)
-  }
-  return v == 1;
-}
 int64_t phase2_workspace_bytes(int, int, int, int, int);
 int phase2_auto_splits(int, int, int64_t, int);
 int phase2_partial(const void*, int, int, int, int, int, int, const void*, const void*, int,
@@ -133,51 +121,57 @@ int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int 
   if (out_dtype != STAR_F32 && out_dtype != STAR_BF16)
     return fail(STAR_ECONFIG, "phase1: unknown out dtype %d", out_dtype);
   if (rc) return rc;
-  if (n_seg < 0 || n_seg > kMaxSegments)
-    return fail(STAR_ECONFIG, "phase1: %d segments per call (max %d)", n_seg, kMaxSegments);
+  if (n_seg < 0) return fail(STAR_ECONFIG, "phase1: %d segments", n_seg);
   if (n_seg == 0) return STAR_OK;
   if (seg_start == nullptr) return fail(STAR_ESHAPE, "phase1: seg_start is NULL");
   if (out == nullptr) return fail(STAR_ESHAPE, "phase1: out is NULL");
   if (q_row_stride < (int64_t)hq * d || kv_row_stride < (int64_t)hkv * d ||
       out_row_stride < (int64_t)hq * d)
     return fail(STAR_ESHAPE, "phase1: row stride smaller than heads*d");
-  SegTable segs;
-  segs.n = n_seg;
+  if (dedup_anchor_rows < 0) return fail(STAR_ECONFIG, "phase1: negative dedup_anchor_rows");
   for (int i = 0; i < n_seg; ++i) {
     int64_t a = seg_start[i], b = seg_start[i + 1];
     if (a < 0 || b < a) return fail(STAR_ESHAPE, "phase1: segment %d has bounds [%lld, %lld)", i,
                                     (long long)a, (long long)b);
     if (b - a > (1ll << 30)) return fail(STAR_ENOTSUP, "phase1: segment longer than 2^30 rows");
-    segs.q_row0[i] = a;
-    segs.k_row0[i] = a;
-    segs.lq[i] = (int32_t)(b - a);
-    segs.lk[i] = (int32_t)(b - a);
-    segs.q_offset[i] = 0;
+    if (dedup_anchor_rows > 0 && b - a < dedup_anchor_rows)
+      return fail(STAR_ESHAPE, "phase1: segment %d shorter than the %lld deduplicated anchor rows",
+                  i, (long long)dedup_anchor_rows);
   }
   const int64_t total = seg_start[n_seg];
   const int64_t lse_stride = total;
   cudaStream_t s = (cudaStream_t)stream;
-  if (dedup_anchor_rows < 0) return fail(STAR_ECONFIG, "phase1: negative dedup_anchor_rows");
-  for (int i = 0; i < n_seg && dedup_anchor_rows > 0; ++i)
-    if (segs.lq[i] < dedup_anchor_rows)
-      return fail(STAR_ESHAPE, "phase1: segment %d shorter than the %lld deduplicated anchor rows",
-                  i, (long long)dedup_anchor_rows);
-  if (dtype == STAR_BF16 && (d == 64 || d == 128)) {
-    if (total >= (1ll << 31)) return fail(STAR_ENOTSUP, "phase1: more than 2^31 rows per call");
-    // only whole 128-row tiles are deduplicated (the tensor-core kernel's q tile); the
-    // fan-out runs in the s128 kernel
-    segs.dedup_tiles = (int32_t)(dedup_anchor_rows / 128);
-    if (segs.dedup_tiles > 0)
-      return phase1_tc(q, k, v, segs, hq, hkv, d, total, q_row_stride, kv_row_stride, out,
-                       out_dtype == STAR_F32, out_row_stride, lse, lse_stride, s);
-    if (d == 128 && (hq / hkv) % 2 == 0 && use_db64())
-      return phase1_tc64(q, k, v, segs, hq, hkv, total, q_row_stride, kv_row_stride, out,
-                         out_dtype == STAR_F32, out_row_stride, lse, lse_stride, s);
-    return phase1_tc(q, k, v, segs, hq, hkv, d, total, q_row_stride, kv_row_stride, out,
+  const bool tc = dtype == STAR_BF16 && (d == 64 || d == 128);
+  if (tc && total >= (1ll << 31)) return fail(STAR_ENOTSUP, "phase1: more than 2^31 rows per call");
+  // The segment table travels in the kernel parameter block (kMaxSegments entries), so a
+  // context with more blocks runs as several stream-ordered launches of up to kMaxSegments
+  // segments each.  Rows stay absolute (same tensors, same tensor maps).  Anchor dedup fans
+  // segment 0's rows out inside its own launch; later launches encode their anchor rows
+  // (identical values, DESIGN §3 f3).
+  for (int c0 = 0; c0 < n_seg; c0 += kMaxSegments) {
+    const int cn = std::min(kMaxSegments, n_seg - c0);
+    SegTable segs;
+    segs.n = cn;
+    for (int i = 0; i < cn; ++i) {
+      const int64_t a = seg_start[c0 + i], b = seg_start[c0 + i + 1];
+      segs.q_row0[i] = a;
+      segs.k_row0[i] = a;
+      segs.lq[i] = (int32_t)(b - a);
+      segs.lk[i] = (int32_t)(b - a);
+      segs.q_offset[i] = 0;
+    }
+    if (tc) {
+      // only whole 128-row tiles are deduplicated (the tensor-core kernel's q tile)
+      segs.dedup_tiles = c0 == 0 ? (int32_t)(dedup_anchor_rows / 128) : 0;
+      rc = phase1_tc(q, k, v, segs, hq, hkv, d, total, q_row_stride, kv_row_stride, out,
                      out_dtype == STAR_F32, out_row_stride, lse, lse_stride, s);
+    } else {
+      rc = attention_simt(q, k, v, dtype, segs, hq, hkv, d, q_row_stride, kv_row_stride, 1, out,
+                          out_dtype, out_row_stride, lse, lse_stride, s);
+    }
+    if (rc) return rc;
   }
-  return attention_simt(q, k, v, dtype, segs, hq, hkv, d, q_row_stride, kv_row_stride, 1, out,
-                        out_dtype, out_row_stride, lse, lse_stride, s);
+  return STAR_OK;
 }
 
 int star_phase1_fwd_range(const void* q, const void* k, const void* v, int dtype, int64_t q_begin,

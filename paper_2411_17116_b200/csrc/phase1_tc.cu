@@ -454,37 +454,10 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
                                  std::max(segs.tile_lo[i], i > 0 ? segs.dedup_tiles : 0);
   const int tiles = prm.segs.tile_start[segs.n];
   if (tiles == 0) return STAR_OK;
-  // tuning knobs (read once): STAR_K1_POLY = share of each S row (in 32-column chunks of 4)
-  // whose exp2 runs on the FMA pipe; STAR_K1_SEQ = softmax ping-pong; STAR_K1_FH = row sum
-  // by f32+bf16 adds (1) or unpack + FADD2 (0)
-  static int poly = -1, seq = -1, fh = -1, onep = -1, spec = -1;
-  if (poly < 0) {
-    const char* env = getenv("STAR_K1_POLY");
-    poly = env ? atoi(env) : kDefaultPoly;
-    if (poly < 0 || poly > 2) poly = kDefaultPoly;
-    env = getenv("STAR_K1_SEQ");
-    seq = env ? (atoi(env) != 0) : kDefaultSeq;
-    env = getenv("STAR_K1_FH");
-    fh = env ? (atoi(env) != 0) : kDefaultFH;
-    env = getenv("STAR_K1_ONEP");
-    onep = env ? (atoi(env) != 0) : kDefaultOnePass;
-    env = getenv("STAR_K1_SPEC");
-    spec = env ? (atoi(env) != 0) : kDefaultSpec;
-  }
-  prm.seq = seq;
-  using KernFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, P1Params);
-  static const KernFn table[2][2][3] = {
-      {{phase1_tc_kernel<D, NQ, 0, false, false>, phase1_tc_kernel<D, NQ, 1, false, false>,
-        phase1_tc_kernel<D, NQ, 2, false, false>},
-       {phase1_tc_kernel<D, NQ, 0, true, false>, phase1_tc_kernel<D, NQ, 1, true, false>,
-        phase1_tc_kernel<D, NQ, 2, true, false>}},
-      {{phase1_tc_kernel<D, NQ, 0, false, true>, phase1_tc_kernel<D, NQ, 1, false, true>,
-        phase1_tc_kernel<D, NQ, 2, false, true>},
-       {phase1_tc_kernel<D, NQ, 0, true, true>, phase1_tc_kernel<D, NQ, 1, true, true>,
-        phase1_tc_kernel<D, NQ, 2, true, true>}}};
-  static const KernFn spec_table[2] = {phase1_tc_kernel<D, NQ, 0, false, 2>,
-                                       phase1_tc_kernel<D, NQ, 0, true, 2>};
-  const KernFn kern = (onep && spec && poly == 0) ? spec_table[fh] : table[onep][fh][poly];
+  // the product build instantiates only the measured-best softmax (one-pass row,
+  // f32 += bf16 row sums, MUFU ping-pong of the two heads, no FMA exp2 share)
+  prm.seq = kDefaultSeq;
+  const auto kern = phase1_tc_kernel<D, NQ, kDefaultPoly, kDefaultFH != 0, kDefaultOnePass>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
   dim3 grid(tiles * hkv * (hq / hkv / NQ));

@@ -289,7 +289,9 @@ __device__ void split_merge_words(int b, int kvh, int r_lo, int r_n, int lq, int
   const int per = (total + nsp - 1) / nsp;
   const int lo = blockIdx.x * per, hi = min(total, lo + per);
   named_barrier_sync(1, NT);  // this CTA's own words are visible to its polls
-  const uint32_t ep = (pp.L.world && lo < hi) ? exchange_epoch(pp) : 0u;
+  // every CTA reads the box epoch, also one whose slice is empty (lo >= hi): it still counts
+  // as an arrival in exchange_merge_slice, and if it arrives last it stores this epoch back
+  const uint32_t ep = pp.L.world ? exchange_epoch(pp) : 0u;
   for (int e = lo + tid; e < hi; e += NT) {
     const int rr = r_lo + e / D, c = e % D;
     const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
@@ -1165,9 +1167,6 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
                 QR);
   int n_rb = QR <= 16 ? 1 : (QR + 63) / 64;  // row blocks (see the kernel)
   dim3 grid(n_splits, hkv * n_rb, batch);
-  // timing experiment only (tools/decode_bench.py): skip the split fix-up (result incomplete)
-  static const bool no_fix = getenv("STAR_K2_EXPERIMENT_NOFIX") != nullptr;
-  if (no_fix) counters = nullptr;
   // split fix-up: word mode (every split CTA polls the others' {value, epoch} words and
   // folds a slice of the group) when the whole grid is co-resident, so no spinning CTA can
   // starve one that has not started; else the arrival-counter fix-up.  STAR_K2_FIXUP=atomic forces the latter (measurement).
@@ -1203,8 +1202,9 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     // the new one.  Zero the header and this launch's partials whenever the workspace's
     // shape or mode changes (stream-ordered; once per change, e.g. query encode -> decode).
     static std::mutex mu;
-    static std::unordered_map<const void*, std::array<int64_t, 6>> last;
-    const std::array<int64_t, 6> sig = {batch, lq, hq, hkv, d,
+    static std::unordered_map<const void*, std::array<int64_t, 7>> last;
+    // n_splits is part of the signature: it moves the lse words and widens the zeroed range
+    const std::array<int64_t, 7> sig = {batch, lq, hq, hkv, d, n_splits,
                                         (grp_epoch != nullptr ? 1 : 0) + (use_qe ? 2 : 0)};
     std::lock_guard<std::mutex> lock(mu);
     auto it = last.find(counters);

@@ -279,6 +279,10 @@ class DistSession:
     last_logits: torch.Tensor | None = None
     generated: list = field(default_factory=list)
     exchange: PeerExchange | None = None  # fused C1 transport; None = all-gather + K3
+    # ranks holding cache rows in phase 2, ascending: the plan's block owners plus the query
+    # rank (fixed once phase 1 is done; no per-token collective needed)
+    nonempty: list = field(default_factory=list)
+    _decoder: object = field(default=None, repr=False)  # decoding.DeviceDecoder
 
 
 def run_phase1_dist(tokens, plan: BlockPlan, spec: AnchorSpec, weights, prng: Prng | None = None,
@@ -316,22 +320,16 @@ def _phase2_forward_dist(sess: DistSession, token_ids, positions, own_tail: int,
     from .model import embed, finish_layer, logits_from, project_qkv
 
     cfg = sess.weights.config
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    rank = dist.get_rank(group)
     x = embed(sess.weights, token_ids)
     pos = list(positions)
     H, hd = cfg.heads, cfg.head_dim
-    nonempty = None
     for li, lw in enumerate(sess.weights.layers):
         q, k, v = project_qkv(x, lw, cfg, pos)
         if rank == sess.q_rank:
             sess.pool.append(li, k, v, pos)
         l = q.shape[0]
         n = sess.pool.rows(li)
-        if nonempty is None:
-            flags = torch.tensor([1 if n else 0], device=q.device)
-            allf = torch.empty(world, dtype=flags.dtype, device=q.device)
-            dist.all_gather_into_tensor(allf, flags, group=group)
-            nonempty = [r for r in range(world) if int(allf[r])]
         qb = q.view(1, l, H, hd).to(sess.pool.dtype).contiguous()
         tail = own_tail if rank == sess.q_rank else 0
         ex = sess.exchange
@@ -341,7 +339,8 @@ def _phase2_forward_dist(sess: DistSession, token_ids, positions, own_tail: int,
             if n:
                 att, _ = ex.exchange(qb, sess.pool.k[li], sess.pool.v[li],
                                      sess.pool.page_table.view(1, -1),
-                                     sess.pool.kv_len_tensor(li), n, own_tail=tail)
+                                     sess.pool.kv_len_tensor(li), n, own_tail=tail,
+                                     workspace=sess.pool.workspace)
                 att = att.view(l * H, hd)
             else:
                 ex.push(torch.zeros(l * H, hd, device=q.device),
@@ -352,14 +351,16 @@ def _phase2_forward_dist(sess: DistSession, token_ids, positions, own_tail: int,
             if n:
                 ops.phase2_partial(qb, sess.pool.k[li], sess.pool.v[li],
                                    sess.pool.page_table.view(1, -1), sess.pool.kv_len_tensor(li),
-                                   n, own_tail=tail, out=o.view(1, l, H, hd), lse=s.view(1, l, H))
+                                   n, own_tail=tail, out=o.view(1, l, H, hd), lse=s.view(1, l, H),
+                                   workspace=sess.pool.workspace)
             else:
                 o.zero_()
                 s.fill_(float("-inf"))
             att, _ = gather_merge(o, s, group=group, packed=packed)
         x = finish_layer(x, att.view(l, H, hd), lw)
     if rank == sess.q_rank:
-        sess.ledger.extend(phase2_ledger_rows(sess.q_rank, nonempty, cfg.layers, H, len(pos), hd))
+        sess.ledger.extend(phase2_ledger_rows(sess.q_rank, sess.nonempty, cfg.layers, H, len(pos),
+                                              hd))
     return logits_from(sess.weights, x)
 
 
@@ -384,6 +385,7 @@ def start_session_dist(weights, tokens, plan: BlockPlan, spec: AnchorSpec, prng=
     shard, pool = run_phase1_dist(tokens[:L], plan, spec, weights, prng, group)
     q_rank = world - 1 if q_rank is None else q_rank
     sess = DistSession(weights, plan, shard, pool, q_rank)
+    sess.nonempty = [r for r in range(world) if plan.blocks_of(r) or r == q_rank]
     if transport == "peer":
         cfg = weights.config
         # capacity: the query encode's l_q rows x heads (decode steps use a prefix of it)
@@ -403,18 +405,49 @@ def start_session_dist(weights, tokens, plan: BlockPlan, spec: AnchorSpec, prng=
     return logits, sess
 
 
-def decode_dist(sess: DistSession, n_tokens: int, group=None) -> list[int]:
-    """Distributed greedy decode (ss/sim.py:340-368); every rank derives the same token."""
+def decode_dist(sess: DistSession, n_tokens: int, group=None, graph: bool | None = None) -> list[int]:
+    """Distributed greedy decode (ss/sim.py:340-368); every rank derives the same token.
+
+    The per-token step runs on the device (decoding.DeviceDecoder) and is graph-captured
+    when the transport allows it (the peer exchange, or NCCL collectives; a gloo group runs
+    the same device step eagerly).  No collective or host sync per token: the ids are read
+    back once per call."""
+    from .decoding import DeviceDecoder, paged_attend
+
+    if n_tokens <= 0:
+        return []
     world = dist.get_world_size(group)
-    out = []
-    for _ in range(n_tokens):
-        t = int(torch.argmax(sess.last_logits))
-        out.append(t)
-        sess.generated.append(t)
-        if dist.get_rank(group) == sess.q_rank:
+    rank = dist.get_rank(group)
+    cfg = sess.weights.config
+    if graph is None:
+        graph = sess.exchange is not None or dist.get_backend(group) == "nccl"
+    dec = sess._decoder
+    if dec is None or dec.remaining() < n_tokens or dec.use_graph != graph:
+        rows = sess.pool.rows(0)
+        room = -(-max(n_tokens, 64) // 64) * 64 if rank == sess.q_rank else 0
+        if room:
+            sess.pool.reserve(rows + room, exact=True)
+        # every rank sizes its decoder for the same token budget
+        budget = -(-max(n_tokens, 64) // 64) * 64
+        attend = paged_attend(sess.pool, appends=rank == sess.q_rank,
+                              max_rows=rows + room if rank in sess.nonempty else 0,
+                              theta=cfg.rope_theta, heads=cfg.heads, exchange=sess.exchange,
+                              group=group)
+        dec = DeviceDecoder(sess.weights, sess.last_logits, sess.next_position, attend, budget,
+                            graph)
+        sess._decoder = dec
+    out = dec.run(n_tokens)
+    p0 = sess.next_position
+    if rank == sess.q_rank:
+        for li in range(cfg.layers):
+            sess.pool.layer_rows[li] += n_tokens
+        sess.pool.positions.extend(range(p0, p0 + n_tokens))
+        for _ in out:
             sess.ledger += [(2, sess.q_rank, r, "query_broadcast", 1) for r in range(world)
                             if r != sess.q_rank]
-        logits = _phase2_forward_dist(sess, [t], [sess.next_position], 0, group)
-        sess.last_logits = logits[-1]
-        sess.next_position += 1
+            sess.ledger.extend(phase2_ledger_rows(sess.q_rank, sess.nonempty, cfg.layers,
+                                                  cfg.heads, 1, cfg.head_dim))
+    sess.generated.extend(out)
+    sess.next_position += n_tokens
+    sess.last_logits = dec.logits
     return out

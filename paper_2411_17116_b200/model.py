@@ -126,21 +126,22 @@ def _positions_tensor(positions, device) -> torch.Tensor:
     return torch.tensor(list(positions), dtype=torch.int64, device=device)
 
 
-def project_qkv(x: torch.Tensor, lw: LayerWeights, cfg: ModelConfig, positions):
-    """RMSNorm -> Q/K/V projections -> RoPE on q and k: ([rows, H, hd] x 3), attention dtype."""
+def project_raw(x: torch.Tensor, lw: LayerWeights, cfg: ModelConfig):
+    """RMSNorm -> Q/K/V projections, before RoPE: ([rows, H, hd] x 3), attention dtype."""
     H, hd = cfg.heads, cfg.head_dim
     xn = _rms_norm(x, lw.attn_gain)
     rows = x.shape[0]
-    q = (xn @ lw.wq).view(rows, H, hd)
-    k = (xn @ lw.wk).view(rows, H, hd)
-    v = (xn @ lw.wv).view(rows, H, hd)
-    pos = _positions_tensor(positions, x.device)
-    if pos.numel() != rows:
-        raise ConfigError(f"{pos.numel()} positions for {rows} rows")
     dt = default_dtype()
-    q = ops.rope(q.to(dt).contiguous(), pos, cfg.rope_theta)
-    k = ops.rope(k.to(dt).contiguous(), pos, cfg.rope_theta)
-    return q, k, v.to(dt).contiguous()
+    return tuple((xn @ w).view(rows, H, hd).to(dt).contiguous() for w in (lw.wq, lw.wk, lw.wv))
+
+
+def project_qkv(x: torch.Tensor, lw: LayerWeights, cfg: ModelConfig, positions):
+    """RMSNorm -> Q/K/V projections -> RoPE on q and k: ([rows, H, hd] x 3), attention dtype."""
+    q, k, v = project_raw(x, lw, cfg)
+    pos = _positions_tensor(positions, x.device)
+    if pos.numel() != x.shape[0]:
+        raise ConfigError(f"{pos.numel()} positions for {x.shape[0]} rows")
+    return ops.rope(q, pos, cfg.rope_theta), ops.rope(k, pos, cfg.rope_theta), v
 
 
 def finish_layer(x: torch.Tensor, att: torch.Tensor, lw: LayerWeights) -> torch.Tensor:

@@ -66,6 +66,27 @@ class RopeConfig:
             raise ConfigError(f"rope theta_base must be positive, got {self.theta_base}")
 
 
+def rope_apply(x, positions, cfg: RopeConfig) -> torch.Tensor:
+    """Rotate adjacent coordinate pairs of each row by its position's angles
+    (ss/numerics.py:161-180): pair i of a row at position p turns by p * theta^(-2i/d), angles
+    in fp64.  x: one head's [rows, head_dim] (numpy / Tensor2D / torch); returns a device
+    tensor in the build precision (star_rope)."""
+    from . import ops
+    from .blocking import _as_device_2d
+    from .errors import ShapeError
+
+    t = _as_device_2d(x)
+    if t.shape[1] != cfg.head_dim:
+        raise ShapeError(f"rope input has {t.shape[1]} cols, config head_dim {cfg.head_dim}")
+    pos = torch.as_tensor(np.asarray(positions, dtype=np.int64).reshape(-1)).to(t.device)
+    if pos.numel() != t.shape[0]:
+        raise ShapeError(f"{pos.numel()} positions for {t.shape[0]} rows")
+    if t.shape[0] == 0:
+        return t.clone()
+    return ops.rope(t.contiguous().view(t.shape[0], 1, t.shape[1]), pos,
+                    cfg.theta_base).view(t.shape)
+
+
 _M64 = (1 << 64) - 1
 _GOLDEN = 0x9E3779B97F4A7C15
 

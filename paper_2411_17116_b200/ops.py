@@ -51,9 +51,13 @@ def _rows_view(t: torch.Tensor, name: str) -> tuple[int, int, int]:
 
 # ---------------------------------------------------------------------------- prng
 def prng_fill(shape, seed: int, first: int = 1, scale: float = 1.0, dtype=torch.float32,
-              device="cuda") -> torch.Tensor:
-    """Draws first..first+n-1 of splitmix64 stream `seed` as (2u-1)*scale (ss/numerics.py:255-263)."""
-    out = torch.empty(shape, dtype=dtype, device=device)
+              device="cuda", out: torch.Tensor | None = None) -> torch.Tensor:
+    """Draws first..first+n-1 of splitmix64 stream `seed` as (2u-1)*scale (ss/numerics.py:255-263).
+    out: fill this contiguous tensor in place (shape/dtype/device taken from it)."""
+    if out is None:
+        out = torch.empty(shape, dtype=dtype, device=device)
+    elif not out.is_contiguous():
+        raise ShapeError("prng_fill out must be contiguous")
     _cuda(out)
     _lib.call("star_prng_fill", out.data_ptr(), dtype_code(out), out.numel(),
               int(seed) & ((1 << 64) - 1), int(first) & ((1 << 64) - 1), float(scale),
@@ -244,6 +248,8 @@ class Phase2Workspace:
         return self.buf.data_ptr()
 
 
+# default workspaces, one per (device, stream): the split-arrival counters and word-mode
+# epochs in a workspace are only safe for stream-ordered launches, so two streams never share one
 _default_ws: dict = {}
 
 
@@ -283,7 +289,7 @@ def _phase2_args(q, k_pages, v_pages, page_table, kv_len, max_kv_len, own_tail, 
     if lse is None:
         lse = torch.empty((B, lq, hq), dtype=torch.float32, device=q.device)
     nbytes = lib.star_phase2_workspace_bytes(B, lq, hq, d, n_splits)
-    ws = workspace or _default_ws.setdefault(q.device, Phase2Workspace())
+    ws = workspace or _default_ws.setdefault((q.device, _stream(q.device)), Phase2Workspace())
     args = (q.data_ptr(), dtype_code(q), B, lq, hq, hkv, d, k_pages.data_ptr(), v_pages.data_ptr(),
             dtype_code(k_pages), k_pages.shape[0], page_table.data_ptr(), pps, page_size,
             kv_len.data_ptr(), int(max_kv_len), int(own_tail), out.data_ptr(), lse.data_ptr(), int(n_splits),

@@ -287,6 +287,7 @@ class DecodeSession:
     next_position: int
     last_logits: torch.Tensor
     generated: list = field(default_factory=list)
+    _decoder: object = field(default=None, repr=False)  # decoding.DeviceDecoder, built lazily
 
 
 def start_session(weights: ModelWeights, tokens, plan: BlockPlan, spec: AnchorSpec,
@@ -321,21 +322,71 @@ def forward_star(weights: ModelWeights, tokens, plan: BlockPlan, spec: AnchorSpe
     return logits
 
 
-def decode(session: DecodeSession, n_tokens: int, greedy: bool = True) -> list[int]:
-    """Greedy decode, one phase-2 step per token (ss/sim.py:340-368)."""
+def _device_attend(hosts, qh: Host, max_rows: dict, theta: float):
+    """Graph-safe phase-2 attention of one decode token (DeviceDecoder.attend_layer): append to
+    the query host on the device, K2 on every non-empty host's pages with the device row
+    counts, merge in ascending host order (ss/sim.py:254-281, :178-213)."""
+
+    def attend(li, q, k, v, pos):
+        qr = qh.pool.append_rope(li, q, k, v, pos, theta)
+        H, hd = qr.shape[1], qr.shape[2]
+        q4 = qr.view(1, 1, H, hd)
+        parts = []
+        for host in hosts:
+            if max_rows[host.index] == 0:
+                continue
+            pool = host.pool
+            o, s = ops.phase2_partial(q4, pool.k[li], pool.v[li], pool.page_table.view(1, -1),
+                                      pool.kv_len_tensor(li), max_rows[host.index],
+                                      workspace=pool.workspace)
+            parts.append((host, o[0], s[0]))
+        return _merge_parts(parts, 1, H, hd)
+
+    return attend
+
+
+def decode(session: DecodeSession, n_tokens: int, greedy: bool = True,
+           graph: bool = True) -> list[int]:
+    """Greedy decode, one phase-2 step per token (ss/sim.py:340-368).
+
+    The step runs on the device (decoding.DeviceDecoder): argmax, embedding, append to the
+    query host, K2 on every host, merge and the next logits, captured once in a CUDA graph
+    and replayed per token; the ids come back in one read at the end.  The ledger gets the
+    reference's rows (query broadcast, then per layer/head/non-query host the partials).
+    """
+    from .decoding import DeviceDecoder
+
     if not greedy:
         raise ConfigError("only greedy decoding is supported")
-    qh = _query_host(session.hosts)
-    new_tokens: list[int] = []
-    for _ in range(n_tokens):
-        t = int(torch.argmax(session.last_logits))
-        new_tokens.append(t)
-        session.generated.append(t)
-        for h in session.hosts:
+    if n_tokens <= 0:
+        return []
+    hosts = session.hosts
+    qh = _query_host(hosts)
+    cfg = session.weights.config
+    dec = session._decoder
+    if dec is None or dec.remaining() < n_tokens or dec.use_graph != graph:
+        rows = qh.pool.rows(0)
+        room = -(-max(n_tokens, 64) // 64) * 64
+        qh.pool.reserve(rows + room, exact=True)
+        max_rows = {h.index: h.pool.rows(0) for h in hosts}
+        max_rows[qh.index] = rows + room
+        dec = DeviceDecoder(session.weights, session.last_logits, session.next_position,
+                            _device_attend(hosts, qh, max_rows, cfg.rope_theta), room, graph)
+        session._decoder = dec
+    new_tokens = dec.run(n_tokens)
+    # host mirror of what the device step did
+    p0 = session.next_position
+    for li in range(cfg.layers):
+        qh.pool.layer_rows[li] += n_tokens
+    qh.pool.positions.extend(range(p0, p0 + n_tokens))
+    nonempty = [(h, None, None) for h in hosts if h.pool.rows(0) > 0]
+    for _ in new_tokens:
+        for h in hosts:
             if h is not qh:
                 session.ledger.append(2, qh.index, h.index, QUERY_BROADCAST, 1)
-        logits = _phase2_forward(session.hosts, session.weights, [t], [session.next_position], 0,
-                                 session.ledger)
-        session.last_logits = logits[-1]
-        session.next_position += 1
+        for _li in range(cfg.layers):
+            _meter(session.ledger, qh, nonempty, 1, cfg.head_dim, cfg.heads)
+    session.generated.extend(new_tokens)
+    session.next_position += n_tokens
+    session.last_logits = dec.logits
     return new_tokens

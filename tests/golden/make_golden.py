@@ -14,7 +14,13 @@ Every fixture names the reference entry point that produced it:
                  merge_partials / streaming_causal_attention (ss/attention.py:109-210)
   blocking.json  blocking.partition / augment       (ss/blocking.py:49-236)
   model_*.npz    sim.start_session + sim.decode on seeded toy models
-                 (ss/sim.py:126-368, ss/toy_model.py:93-196, ss/cli.py:108-228)
+                 (ss/sim.py:126-368, ss/toy_model.py:93-196, ss/cli.py:108-228);
+                 model_anc_*.npz: the same under every non-default anchor mode
+                 (ss/blocking.py:182-236)
+  encode_block.npz  blocking.encode_block          (ss/blocking.py:239-265)
+
+`python tests/golden/make_golden.py NAME...` regenerates only the named fixtures
+(prng rope attention blocking encode_block model_<case>).
 """
 
 from __future__ import annotations
@@ -201,10 +207,57 @@ MODEL_CASES = {
 }
 
 
+# every non-default anchor mode through the whole protocol (phase 1 anchors -> caches ->
+# phase 2 -> greedy tokens): 4 hosts, one block each, b = 64, a = 32
+_ANC = dict(d_model=64, heads=2, layers=2, L=256, b=64, a=32, H=4, lq=6, ng=8)
+for _name, _cm, _pm, _seed in (("anc_prev", "previous_block", "previous_block", 11),
+                               ("anc_randpos", "first_block", "random_sampled", 12),
+                               ("anc_prevpos", "first_block", "previous_block", 13),
+                               ("anc_shuffled", "shuffled_first_block", "first_block", 14),
+                               ("anc_randtok", "random_tokens", "first_block", 15),
+                               ("anc_const", "constant_token", "first_block", 16),
+                               ("anc_none", "none", "first_block", 17)):
+    MODEL_CASES[_name] = dict(_ANC, seed=_seed,
+                              anchor={"anchor_len": _ANC["a"], "content_mode": _cm,
+                                      "position_mode": _pm, "constant_token_id": 7,
+                                      "token_range": 256})
+
+
+def gen_encode_block():
+    """encode_block over every augmented block of a small plan (first-block anchors and the
+    previous-block mode), fp32: the own-row K/V cache and its positions."""
+    from starsim.blocking import AnchorSpec, augment, encode_block, partition
+
+    rng = np.random.default_rng(21)
+    d_model, hd = 32, 16
+    out = {}
+    with precision("float32"):
+        emb = Tensor2D(rng.uniform(-1, 1, (256, d_model)).astype(np.float32))
+        wq, wk, wv = (Tensor2D(rng.uniform(-0.3, 0.3, (d_model, hd)).astype(np.float32))
+                      for _ in range(3))
+        tokens = [int(t) for t in rng.integers(0, 256, 50)]
+        for mode in ("first_block", "previous_block"):
+            plan = partition(50, 16, 2)
+            spec = AnchorSpec(mode, mode, 8)
+            blocks = augment(plan, tokens, spec, Prng(5))
+            for bl in blocks:
+                c = encode_block(bl, emb, wq, wk, wv, RopeConfig(hd, 10000.0), host=1)
+                key = f"{mode}_{bl.block_index}"
+                out[f"{key}_token_ids"] = np.array(bl.token_ids, dtype=np.int64)
+                out[f"{key}_position_ids"] = np.array(bl.position_ids, dtype=np.int64)
+                out[f"{key}_anchor"] = np.array(bl.anchor_prefix_len)
+                out[f"{key}_k"], out[f"{key}_v"] = c.keys.a, c.values.a
+                out[f"{key}_pos"] = np.array(c.positions, dtype=np.int64)
+            out[f"{mode}_n"] = np.array(len(blocks))
+        out["embedding"], out["wq"], out["wk"], out["wv"] = emb.a, wq.a, wk.a, wv.a
+    np.savez(os.path.join(HERE, "encode_block.npz"), **out)
+
+
 def run_model_case(name, c, with_global=False):
     doc = {
         "model": {"d_model": c["d_model"], "heads": c["heads"], "layers": c["layers"], "seed": c["seed"]},
-        "sequence_len": c["L"], "block_size": c["b"], "anchor": {"anchor_len": c["a"]},
+        "sequence_len": c["L"], "block_size": c["b"],
+        "anchor": c.get("anchor", {"anchor_len": c["a"]}),
         "hosts": c["H"], "query_len": c["lq"], "n_generate": c["ng"], "seed": c.get("data_seed", 0),
     }
     cfg = cli.build_experiment(doc)
@@ -249,15 +302,18 @@ def run_model_case(name, c, with_global=False):
     return gen, margins
 
 
-def main():
-    gen_prng()
-    gen_rope()
-    gen_attention()
-    gen_blocking()
+def main(names=None):
+    gens = {"prng": gen_prng, "rope": gen_rope, "attention": gen_attention,
+            "blocking": gen_blocking, "encode_block": gen_encode_block}
+    for key, fn in gens.items():
+        if not names or key in names:
+            fn()
     for name, c in MODEL_CASES.items():
+        if names and f"model_{name}" not in names:
+            continue
         gen, margins = run_model_case(name, c, with_global=c["L"] <= 128)
         print(name, gen, "min margin %.3g" % min(margins))
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])

@@ -48,8 +48,8 @@ def test_status_maps_to_reference_exceptions():
     assert rc == _lib.STAR_ESHAPE  # hq not a multiple of hkv
     with pytest.raises(ShapeError):
         _lib.check(rc)
-    rc = lib.star_phase1_fwd(None, None, None, 0, 99, seg, 4, 4, 8, 32, 32, None, 0, 32, None, 0, None)
-    with pytest.raises(ConfigError):
+    rc = lib.star_phase1_fwd(None, None, None, 0, -1, seg, 4, 4, 8, 32, 32, None, 0, 32, None, 0, None)
+    with pytest.raises(ConfigError):  # a negative segment count (any positive count is chunked)
         _lib.check(rc)
     rc = lib.star_rope(None, None, 0, 4, 1, 7, 7, 7, None, 10000.0, None)
     with pytest.raises(ConfigError, match="even"):

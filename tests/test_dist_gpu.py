@@ -1,7 +1,9 @@
-"""Distributed session (paper_2411_17116_b200.dist) on the B200: 2-4 ranks share cuda:0.
+"""Distributed session (paper_2411_17116_b200.dist) on the B200.
 
-NCCL refuses two ranks on one device, so the process group here is gloo over CUDA
-tensors; the kernels (K1/K2/K3) are the real ones.  transport="peer" runs the fused
+backend "gloo": 2-4 ranks share cuda:0 (NCCL refuses two ranks on one device), so the process
+group is gloo over CUDA tensors; the kernels (K1/K2/K3) are the real ones.
+backend "nccl": one rank per device (cuda:rank), NCCL process group and cross-device CUDA IPC
+for the peer boxes — the production layout; skipped when fewer devices than ranks exist.  transport="peer" runs the fused
 exchange: each process maps the other's box through CUDA IPC (two contexts on one
 device; the GPU time-slices them while K3x waits for the other rank's flags).  Checked against the
 reference's 2-host golden: identical greedy tokens and ledger, logits within
@@ -31,19 +33,24 @@ def _port():
     return p
 
 
-def _worker(rank, port, name, q, transport, world, dtype="float32"):
+def _worker(rank, port, name, q, transport, world, dtype="float32", backend="gloo"):
     import sys
 
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2411_17116_b200 as S
         from paper_2411_17116_b200 import dist as D
 
-        torch.cuda.set_device(0)
         torch.backends.cuda.matmul.allow_tf32 = False
         S.set_default_dtype(dtype)
         g = np.load(os.path.join(GOLDEN, f"model_{name}.npz"))
@@ -57,6 +64,7 @@ def _worker(rank, port, name, q, transport, world, dtype="float32"):
         logits, sess = D.start_session_dist(w, toks, plan, spec, prng=S.Prng(doc["seed"] ^ 0xA17C4B10C4ED5EED),
                                             transport=transport)
         gen = D.decode_dist(sess, doc["n_generate"])
+        transport_used = "peer" if sess.exchange is not None else "collective"
         if sess.exchange is not None:
             dist.barrier()  # every rank done with the others' boxes
             sess.exchange.close()
@@ -75,7 +83,7 @@ def _worker(rank, port, name, q, transport, world, dtype="float32"):
             csv = "phase,src,dst,kind,scalar_count\n" + "".join(
                 f"{a},{b},{c},{k},{n}\n" for a, b, c, k, n in sess.ledger)
         q.put((rank, {"gen": gen, "ref": [int(t) for t in g["generated"]], "err": err, "csv": csv,
-                      "sim": sim,
+                      "sim": sim, "transport": transport_used,
                       "ref_csv": str(g["ledger_csv"]),
                       "pos": list(sess.pool.positions),
                       "ref_pos": [int(p) for p in g[f"host{rank}_pos_ch0"]]}))
@@ -86,20 +94,26 @@ def _worker(rank, port, name, q, transport, world, dtype="float32"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,transport,dtype", [
-    ("small_n2", "collective", "float32"), ("small_n2", "peer", "float32"),
-    ("small_n5h2", "collective", "float32"), ("small_n5h2", "peer", "float32"),
-    ("small_n4h4", "peer", "float32"),   # 4 ranks
-    ("tiny_s0", "peer", "float32"),      # BASELINE configs[0]: 4 hosts, 4K context, 16 tokens
-    ("tiny_s0", "peer", "bfloat16"),     # tensor-core path: one-kernel fused exchange per layer
+@pytest.mark.parametrize("name,transport,dtype,backend", [
+    ("small_n2", "collective", "float32", "gloo"), ("small_n2", "peer", "float32", "gloo"),
+    ("small_n5h2", "collective", "float32", "gloo"), ("small_n5h2", "peer", "float32", "gloo"),
+    ("small_n4h4", "peer", "float32", "gloo"),   # 4 ranks
+    ("tiny_s0", "peer", "float32", "gloo"),      # BASELINE configs[0]: 4 hosts, 4K ctx, 16 tokens
+    ("tiny_s0", "peer", "bfloat16", "gloo"),     # tensor cores: one-kernel fused exchange
+    # one rank per GPU over NCCL (cross-device IPC boxes / NCCL all-gather, graph-captured)
+    ("small_n2", "peer", "float32", "nccl"), ("small_n2", "collective", "float32", "nccl"),
+    ("tiny_s0", "peer", "bfloat16", "nccl"), ("tiny_s0", "collective", "float32", "nccl"),
 ])
-def test_dist_session_ranks(name, transport, dtype):
+def test_dist_session_ranks(name, transport, dtype, backend):
     g = np.load(os.path.join(GOLDEN, f"model_{name}.npz"))
     world = int(json.loads(str(g["doc"]))["hosts"])
+    if backend == "nccl" and torch.cuda.device_count() < world:
+        pytest.skip(f"{world} ranks over NCCL need {world} GPUs "
+                    f"({torch.cuda.device_count()} visible)")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, port, name, q, transport, world, dtype))
+    procs = [ctx.Process(target=_worker, args=(r, port, name, q, transport, world, dtype, backend))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -110,6 +124,7 @@ def test_dist_session_ranks(name, transport, dtype):
         res = out[r]
         assert "error" not in res, res
         assert res["pos"] == res["ref_pos"]
+        assert res["transport"] == transport, res["transport"]  # no silent fallback
         if dtype == "float32":
             assert res["gen"] == res["ref"]
             assert res["err"] < 1e-4

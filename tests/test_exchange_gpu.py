@@ -163,23 +163,29 @@ def test_exchange_rejects_oversized_call(mods):
         exs[0].push(o, s, 1, 4, 4, 2)
 
 
-@pytest.mark.parametrize("world,splits,hq,hkv,lq_q", [(1, 0, 8, 2, 4), (3, 2, 8, 2, 4),
-                                                    (2, 3, 8, 2, 4), (8, 2, 8, 2, 4),
-                                                    (2, 2, 32, 8, 32), (1, 0, 32, 8, 32)])
-def test_fused_exchange_one_kernel(mods, world, splits, hq, hkv, lq_q):
+@pytest.mark.parametrize("world,splits,hq,hkv,lq_q,d", [(1, 0, 8, 2, 4, 128), (3, 2, 8, 2, 4, 128),
+                                                        (2, 3, 8, 2, 4, 128), (8, 2, 8, 2, 4, 128),
+                                                        (2, 2, 32, 8, 32, 128), (1, 0, 32, 8, 32, 128),
+                                                        # MHA, d = 64, one query row: 64 output
+                                                        # elements over 9 / 17 splits leave the
+                                                        # last splits' fold slices empty
+                                                        (2, 9, 2, 2, 1, 64), (3, 17, 2, 2, 1, 64)])
+def test_fused_exchange_one_kernel(mods, world, splits, hq, hkv, lq_q, d):
     """star_phase2_exchange: partial + push + cross-rank merge in ONE K2 launch per rank
     (co-resident word-mode grid).  Ranks run on separate streams of one GPU with small grids
     (world x splits x hkv CTAs all resident), as they would on separate GPUs; bit-exact
-    against the unfused K2 + K3 merge, and against plain K2 for one rank."""
+    against the unfused K2 + K3 merge, and against plain K2 for one rank.  Ten steps, so a
+    CTA with an empty fold slice arriving last (it must still carry the box epoch) shows up."""
     ops, D = mods
-    d, ps = 128, 64
+    ps = 64
     lens = [2000, 1500, 2600, 900, 3100, 1700, 2222, 1300][:world]
     caches = _rank_caches(lens, hkv, d, torch.bfloat16, ps, seed=21 + world)
     _write(ops, caches)
     exs = D.local_peer_exchanges(world, lq_q * hq, hkv, d, "cuda")
     streams = [torch.cuda.Stream() for _ in range(world)]
     g = torch.Generator().manual_seed(3)
-    for lq, tail in ((lq_q, lq_q), (1, 0), (1, 0)):
+    steps = [(lq_q, lq_q)] + [(1, 0)] * (2 if d == 128 else 9)
+    for lq, tail in steps:
         q = torch.randn(1, lq, hq, d, generator=g).to(torch.bfloat16).cuda()
         torch.cuda.synchronize()
         outs = [None] * world

@@ -380,3 +380,34 @@ def test_phase1_query_range(ops, d, hq, hkv, dtype):
         from paper_2411_17116_b200.errors import ConfigError
         with pytest.raises(ConfigError):
             ops.phase1_fwd_range(q, k, v, 100, 300, out=got)  # not a whole q tile
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_phase1_more_segments_than_one_launch(ops, dtype):
+    """A context with more blocks than one launch's segment table (kMaxSegments = 64) runs
+    as several launches: every segment equals its own single-segment encode (bit-exact),
+    and anchor dedup across the launch boundary equals the full encode."""
+    hq, hkv, d, a = 4, 2, 64, 128
+    n = 70
+    own = [128 + 64 * (i % 3) for i in range(n)]
+    seg = [0]
+    for i, o in enumerate(own):
+        seg.append(seg[-1] + o + (a if i else 0))
+    rows = seg[-1]
+    q = ops.prng_fill((rows, hq, d), 41, 1, 1.0, dtype, "cuda")
+    k = ops.prng_fill((rows, hkv, d), 42, 1, 1.0, dtype, "cuda")
+    v = ops.prng_fill((rows, hkv, d), 43, 1, 1.0, dtype, "cuda")
+    for s in range(1, n):  # first-block anchors
+        for t in (q, k, v):
+            t[seg[s]:seg[s] + a] = t[:a]
+    full, full_l = ops.phase1_fwd(q, k, v, seg, want_lse=True)
+    for s in (0, 1, 63, 64, 69):
+        b, e = seg[s], seg[s + 1]
+        one, one_l = ops.phase1_fwd(q[b:e].contiguous(), k[b:e].contiguous(), v[b:e].contiguous(),
+                                    [0, e - b], want_lse=True)
+        assert torch.equal(full[b:e], one), s
+        assert torch.equal(full_l[:, b:e], one_l), s
+    if dtype == torch.bfloat16:
+        dd, dd_l = ops.phase1_fwd(q, k, v, seg, want_lse=True, dedup_anchor_rows=a)
+        torch.cuda.synchronize()
+        assert torch.equal(full, dd) and torch.equal(full_l, dd_l)

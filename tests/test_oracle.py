@@ -119,6 +119,9 @@ def test_blocking(golden_dir):
 
 SMALL = ["small_n2", "small_n5h2", "small_n4h4"]
 TINY = ["tiny_s0", "tiny_s4", "tiny_s7"]
+# every non-default anchor mode through the whole protocol (make_golden.py MODEL_CASES)
+ANCHOR = ["anc_prev", "anc_randpos", "anc_prevpos", "anc_shuffled", "anc_randtok", "anc_const",
+          "anc_none"]
 
 
 def _run_case(golden_dir, name):
@@ -130,12 +133,12 @@ def _run_case(golden_dir, name):
     ctx, qry = O.experiment_tokens(doc["seed"], doc["sequence_len"], doc["query_len"])
     assert ctx == list(g["context_tokens"]) and qry == list(g["query_tokens"])
     plan = O.plan_blocks(doc["sequence_len"], doc["block_size"], doc["hosts"])
-    spec = O.Anchor(anchor_len=doc["anchor"]["anchor_len"])
+    spec = O.Anchor(**doc["anchor"])
     lg, sess = O.start_session(m, ctx + qry, plan, spec, O.OraclePrng(doc["seed"] ^ O.ANCHOR_SALT))
     return g, doc, m, lg, sess
 
 
-@pytest.mark.parametrize("name", SMALL + TINY)
+@pytest.mark.parametrize("name", SMALL + TINY + ANCHOR)
 def test_model_end_to_end(golden_dir, name):
     g, doc, m, lg, sess = _run_case(golden_dir, name)
     np.testing.assert_allclose(lg, g["query_logits"], rtol=1e-4, atol=1e-5)
