@@ -745,47 +745,99 @@ def decode_layers_step(dev, world, rank, own_rows, ex, k2_us, barrier, max_over_
     return res
 
 
-def decode_sweep(dev, hq, hkv, d, hbm_peak):
-    """BASELINE configs[4] on one GPU: K2 per-token latency per layer over batch x cached
-    tokens (one layer's paged cache; B x S beyond HBM for 32 layers)."""
+def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
+    """BASELINE configs[4]: batch B in {1..32} x 64 generated tokens over S in {32K..1M}
+    cached tokens, split-KV + LSE merge at G in {1, 2, 4, 8} ranks, one layer.
+
+    A rank holds S/G cached rows per sequence, so the per-rank work of (B, S, G) is the
+    (B, S/G) point: per token, star_kv_append of the B new rows (the query rank's append,
+    device counters) + K2 over the B sequences' paged caches, captured in one CUDA graph and
+    replayed for the 64 generated tokens (the caches grow by one row per token).  For G > 1
+    the cross-rank combine is the merge of G (out, lse) partials, timed here as K3 over G
+    parts (its NVLink transport is the peer exchange).  Points whose per-rank
+    cache exceeds cap_gib are skipped (B = 32 x 1M at G = 1 is 128 GiB)."""
     import torch
 
     from paper_2411_17116_b200 import ops
 
+    page = 128
+    Bs, Ss, Gs = (1, 2, 4, 8, 16, 32), (32768, 131072, 262144, 1048576), (1, 2, 4, 8)
+    kern = {}
+    for B in Bs:
+        for rows in sorted({S // G for S in Ss for G in Gs}):
+            gib = B * rows * hkv * d * 2 * 2 / 2 ** 30
+            if gib > cap_gib:
+                continue
+            pps = -(-(rows + n_tokens) // page)
+            kp = torch.empty((B * pps, hkv, page, d), dtype=torch.bfloat16, device=dev)
+            vp = torch.empty_like(kp)
+            ops.prng_fill(None, 21, out=kp.view(-1))
+            ops.prng_fill(None, 22, out=vp.view(-1))
+            table = torch.arange(B * pps, dtype=torch.int32, device=dev).view(B, pps)
+            q = ops.prng_fill((B, 1, hq, d), 23, 1, 1.0, torch.bfloat16, dev)
+            kn = ops.prng_fill((B, hkv, d), 24, 1, 1.0, torch.bfloat16, dev)
+            vn = ops.prng_fill((B, hkv, d), 25, 1, 1.0, torch.bfloat16, dev)
+            pos = torch.full((B,), rows, dtype=torch.int64, device=dev)
+            kv_len = torch.full((B,), rows, dtype=torch.int32, device=dev)
+            ws = ops.Phase2Workspace()
+            maxk = rows + n_tokens
+
+            def step():
+                qr = ops.kv_append(q.view(B, hq, d), kn, vn, pos, kv_len, kp, vp, table)
+                ops.phase2_partial(qr.view(B, 1, hq, d), kp, vp, table, kv_len, maxk, workspace=ws)
+                pos.add_(1)
+
+            step()
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+                step()
+            torch.cuda.current_stream(dev).wait_stream(side)
+            kv_len.fill_(rows)
+            pos.fill_(rows)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(n_tokens):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            us = e0.elapsed_time(e1) / n_tokens * 1e3
+            nbytes = B * (rows + n_tokens / 2) * hkv * d * 2 * 2  # mean cache over the 64 tokens
+            kern[(B, rows)] = (us, nbytes / us / 1e3)
+            del kp, vp, g
+            torch.cuda.empty_cache()
+    merge_us = {}
+    for B in Bs:
+        for G in Gs[1:]:
+            outs = ops.prng_fill((G, B * hq, d), 26, 1, 1.0, torch.float32, dev)
+            lses = ops.prng_fill((G, B * hq), 27, 1, 1.0, torch.float32, dev)
+            ops.merge(outs, lses)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(50):
+                ops.merge(outs, lses)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            merge_us[(B, G)] = e0.elapsed_time(e1) / 50 * 1e3
     out = []
-    for B, S in ((1, 16384), (1, 32768), (1, 131072), (1, 1048576), (8, 131072), (32, 32768)):
-        page = 128
-        pages = B * (S // page)
-        kp = ops.prng_fill((pages, hkv, page, d), 21, 1, 1.0, torch.bfloat16, dev)
-        vp = ops.prng_fill((pages, hkv, page, d), 22, 1, 1.0, torch.bfloat16, dev)
-        table = torch.arange(pages, dtype=torch.int32, device=dev).view(B, -1)
-        q = ops.prng_fill((B, 1, hq, d), 23, 1, 1.0, torch.bfloat16, dev)
-        kv_len = torch.full((B,), S, dtype=torch.int32, device=dev)
-        ws = ops.Phase2Workspace()
-        f = lambda: ops.phase2_partial(q, kp, vp, table, kv_len, S, workspace=ws)  # noqa: E731
-        f()
-        side = torch.cuda.Stream(dev)
-        side.wait_stream(torch.cuda.current_stream(dev))
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
-            for _ in range(10):
-                f()
-        torch.cuda.current_stream(dev).wait_stream(side)
-        g.replay()
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(5):
-            g.replay()
-        e1.record()
-        torch.cuda.synchronize(dev)
-        us = e0.elapsed_time(e1) / 50 * 1e3
-        nbytes = B * S * hkv * d * 2 * 2
-        out.append({"batch": B, "cached_tokens": S, "us_per_token_per_layer": us,
-                    "gbs": nbytes / us / 1e3, "frac_of_measured_hbm": nbytes / us / 1e3 / hbm_peak})
-        del kp, vp, g
-        torch.cuda.empty_cache()
-    return out
+    for B in Bs:
+        for S in Ss:
+            for G in Gs:
+                k = kern.get((B, S // G))
+                if k is None:
+                    out.append({"batch": B, "cached_tokens": S, "ranks": G,
+                                "skipped": f"per-rank cache > {cap_gib:.0f} GiB"})
+                    continue
+                out.append({"batch": B, "cached_tokens": S, "ranks": G, "rows_per_rank": S // G,
+                            "us_per_token_per_layer": k[0], "gbs": k[1],
+                            "frac_of_measured_hbm": k[1] / hbm_peak,
+                            "merge_us": merge_us.get((B, G))})
+    return {"points": out, "tokens": n_tokens,
+            "timing": "per (B, S/G): CUDA graph of star_kv_append (B rows) + K2 over B paged "
+                      "caches, replayed for 64 generated tokens; merge_us = K3 over G partials"}
 
 
 def cfg1_session(dev):

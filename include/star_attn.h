@@ -82,6 +82,24 @@ int star_rope_qkv(const void* q_in, const void* k_in, const void* v_in, int dtyp
                   void* stream);
 
 /*
+ * Decode append (replaces the per-token KVCache.append of the query host,
+ * ss/blocking.py:161-170 via ss/sim.py:275-277, plus rope_apply of the new
+ * rows' q and k, ss/numerics.py:161-180) for `batch` sequences of `rows` new
+ * rows each: RoPE of q [batch*rows, hq, d] and k [batch*rows, hkv, d] at
+ * `positions` (device int64 [batch*rows]); rotated q -> q_out; rotated k and
+ * raw v written at the logical cache rows kv_len[b] + r of sequence b's pages
+ * (page_table [batch, pages_per_seq]), then kv_len[b] += rows.  kv_len is a
+ * DEVICE int32 [batch] counter, so a decode step that calls this is
+ * graph-capturable; the caller keeps kv_len[b] + rows <= pages_per_seq *
+ * page_size (the rows it reserved).
+ */
+int star_kv_append(const void* q_in, const void* k_in, const void* v_in, int dtype, int batch,
+                   int rows, int hq, int hkv, int d, int64_t q_in_stride, int64_t kv_in_stride,
+                   void* q_out, int64_t q_out_stride, const int64_t* positions, double theta,
+                   int32_t* kv_len, void* k_pages, void* v_pages, const int32_t* page_table,
+                   int pages_per_seq, int page_size, void* stream);
+
+/*
  * Phase 1 (K1): causal self-attention over one or more anchor-augmented
  * blocks concatenated along rows.  Segment s covers rows
  * [seg_start[s], seg_start[s+1]) of q/k/v/out (seg_start: HOST array of

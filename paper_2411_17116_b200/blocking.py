@@ -262,20 +262,14 @@ class PagedKVPool:
 
     def append_rope(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                     positions: torch.Tensor, theta: float) -> torch.Tensor:
-        """Graph-safe append of one step's rows (the fused prologue): RoPE of q
-        and k at the device `positions`, rotated k and raw v written at the rows the device
-        counter kv_len_dev[layer] names, counter advanced on the device.  Returns rotated q.
+        """Graph-safe append of one step's rows (star_kv_append, one launch): RoPE of q and k
+        at the device `positions`, rotated k and raw v written at the rows the device counter
+        kv_len_dev[layer] names, counter advanced on the device.  Returns rotated q.
         The host mirror (layer_rows, positions) is the caller's to advance (DeviceDecoder)."""
-        n = k.shape[0]
-        rows = self.kv_len_dev[layer:layer + 1].to(torch.int64)
-        if n > 1:
-            rows = rows + torch.arange(n, dtype=torch.int64, device=self.device)
         dt = self.dtype
-        qo, _ = ops.rope_qkv(q.to(dt).contiguous(), k.to(dt).contiguous(), v.to(dt).contiguous(),
-                             positions, theta, cache_rows=rows, k_pages=self.k[layer],
-                             v_pages=self.v[layer], page_table=self.page_table)
-        self.kv_len_dev[layer:layer + 1] += n
-        return qo
+        return ops.kv_append(q.to(dt).contiguous(), k.to(dt).contiguous(), v.to(dt).contiguous(),
+                             positions, self.kv_len_dev[layer:layer + 1], self.k[layer],
+                             self.v[layer], self.page_table, theta)
 
     def rows(self, layer: int) -> int:
         return self.layer_rows[layer]

@@ -48,6 +48,9 @@ int kv_write(const void*, const void*, int, int64_t, int, int, int64_t, void*, v
 int rope_qkv(const void*, const void*, const void*, int, int64_t, int, int, int, int64_t, int64_t,
              void*, void*, int64_t, int64_t, const int64_t*, double, const int64_t*, void*, void*,
              const int32_t*, int, cudaStream_t);
+int kv_append(const void*, const void*, const void*, int, int, int, int, int, int, int64_t,
+              int64_t, void*, int64_t, const int64_t*, double, int32_t*, void*, void*,
+              const int32_t*, int, int, cudaStream_t);
 int kv_read(const void*, const void*, int, const int32_t*, int, int64_t, int64_t, int, int, void*,
             void*, cudaStream_t);
 int attention_simt(const void*, const void*, const void*, int, SegTable&, int, int, int, int64_t,
@@ -111,6 +114,18 @@ int star_rope_qkv(const void* q_in, const void* k_in, const void* v_in, int dtyp
   return rope_qkv(q_in, k_in, v_in, dtype, rows, hq, hkv, d, q_in_stride, kv_in_stride, q_out,
                   k_out, q_out_stride, k_out_stride, positions, theta, cache_rows, k_pages,
                   v_pages, page_table, page_size, (cudaStream_t)stream);
+}
+
+int star_kv_append(const void* q_in, const void* k_in, const void* v_in, int dtype, int batch,
+                   int rows, int hq, int hkv, int d, int64_t q_in_stride, int64_t kv_in_stride,
+                   void* q_out, int64_t q_out_stride, const int64_t* positions, double theta,
+                   int32_t* kv_len, void* k_pages, void* v_pages, const int32_t* page_table,
+                   int pages_per_seq, int page_size, void* stream) {
+  int rc = check_heads(hq, hkv, d);
+  if (rc) return rc;
+  return kv_append(q_in, k_in, v_in, dtype, batch, rows, hq, hkv, d, q_in_stride, kv_in_stride,
+                   q_out, q_out_stride, positions, theta, kv_len, k_pages, v_pages, page_table,
+                   pages_per_seq, page_size, (cudaStream_t)stream);
 }
 
 int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int n_seg,

@@ -180,6 +180,93 @@ int rope_qkv(const void* qi, const void* ki, const void* vi, int dtype, int64_t 
   return STAR_OK;
 }
 
+// ------------------------------------------------------------------ decode append
+// The per-token append of phase 2 (ss/sim.py:275-277, append-then-attend) with every piece of
+// state on the device, so a decode step is graph-capturable: for each of `batch` sequences,
+// RoPE of its `rows` new rows' q and k at their device positions (the same fp64 angle as
+// rope_kernel), rotated k and raw v written at the cache rows the sequence's device counter
+// kv_len[b] names, counter advanced by `rows`.  One CTA per sequence (its counter is read
+// before and bumped after a CTA barrier).  It triggers its programmatic dependents at entry:
+// the K2 launch that follows (PDL) sets up beside it and waits in griddepcontrol.wait for
+// this kernel's stores.
+template <typename T>
+__global__ void __launch_bounds__(256) kv_append_kernel(
+    const T* __restrict__ qi, const T* __restrict__ ki, const T* __restrict__ vi,
+    T* __restrict__ qo, int rows, int hq, int hkv, int d, int64_t qis, int64_t kis, int64_t qos,
+    const int64_t* __restrict__ pos, double theta, int32_t* __restrict__ kv_len,
+    T* __restrict__ kp, T* __restrict__ vp, const int32_t* __restrict__ page_table, int pps,
+    int page_size) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // no-op unless launched as a dependent
+  const int b = blockIdx.x;
+  const int half = d >> 1;
+  const int64_t base = kv_len[b];
+  const int32_t* table = page_table + (int64_t)b * pps;
+  for (int idx = threadIdx.x; idx < rows * half; idx += blockDim.x) {
+    const int rl = idx / half, i = idx - rl * half;
+    const int64_t r = (int64_t)b * rows + rl;  // row of the q/k/v inputs
+    double sn, cs;
+    sincos((double)pos[r] * pow(theta, -2.0 * (double)i / (double)d), &sn, &cs);
+    const T* q = qi + r * qis + 2 * i;
+    T* qw = qo + r * qos + 2 * i;
+    for (int h = 0; h < hq; ++h) {
+      const double x0 = Elem<T>::to_f(q[h * d]), x1 = Elem<T>::to_f(q[h * d + 1]);
+      qw[h * d] = Elem<T>::from_f(__double2float_rn(x0 * cs - x1 * sn));
+      qw[h * d + 1] = Elem<T>::from_f(__double2float_rn(x0 * sn + x1 * cs));
+    }
+    const int64_t cr = base + rl;
+    const int64_t page = table[cr / page_size];
+    const int64_t slot = cr % page_size;
+    T* kpr = kp + (page * hkv * page_size + slot) * d + 2 * i;
+    T* vpr = vp + (page * hkv * page_size + slot) * d + 2 * i;
+    const T* k = ki + r * kis + 2 * i;
+    const T* v = vi + r * kis + 2 * i;
+    for (int h = 0; h < hkv; ++h) {
+      const double x0 = Elem<T>::to_f(k[h * d]), x1 = Elem<T>::to_f(k[h * d + 1]);
+      const int64_t po = (int64_t)h * page_size * d;
+      kpr[po] = Elem<T>::from_f(__double2float_rn(x0 * cs - x1 * sn));
+      kpr[po + 1] = Elem<T>::from_f(__double2float_rn(x0 * sn + x1 * cs));
+      vpr[po] = v[h * d];
+      vpr[po + 1] = v[h * d + 1];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) kv_len[b] = (int32_t)(base + rows);
+}
+
+int kv_append(const void* qi, const void* ki, const void* vi, int dtype, int batch, int rows,
+              int hq, int hkv, int d, int64_t qis, int64_t kis, void* qo, int64_t qos,
+              const int64_t* pos, double theta, int32_t* kv_len, void* kp, void* vp,
+              const int32_t* table, int pps, int page_size, cudaStream_t s) {
+  if (d < 2 || (d & 1)) return fail(STAR_ECONFIG, "rope head_dim must be even and >= 2, got %d", d);
+  if (!(theta > 0)) return fail(STAR_ECONFIG, "rope theta must be positive, got %g", theta);
+  if (batch < 0 || rows < 0 || hq < 1 || hkv < 1 || page_size < 1 || pps < 1)
+    return fail(STAR_ESHAPE, "kv_append: bad shape");
+  if (qis < (int64_t)hq * d || qos < (int64_t)hq * d || kis < (int64_t)hkv * d)
+    return fail(STAR_ESHAPE, "kv_append: row stride smaller than heads*d");
+  if (kv_len == nullptr || kp == nullptr || vp == nullptr || table == nullptr || pos == nullptr)
+    return fail(STAR_ESHAPE, "kv_append: NULL counter / pool / table / positions");
+  if ((int64_t)rows > (int64_t)pps * page_size)
+    return fail(STAR_ESHAPE, "kv_append: %d rows exceed the %lld rows a page table maps", rows,
+                (long long)pps * page_size);
+  if (batch == 0 || rows == 0) return STAR_OK;
+  // (the counters live on the device: the caller reserves pps * page_size rows per sequence
+  // for the whole decode, DeviceDecoder / PagedKVPool.reserve)
+#define STAR_KVA(T)                                                                                \
+  kv_append_kernel<T><<<batch, 256, 0, s>>>((const T*)qi, (const T*)ki, (const T*)vi, (T*)qo,     \
+                                            rows, hq, hkv, d, qis, kis, qos, pos, theta, kv_len,   \
+                                            (T*)kp, (T*)vp, table, pps, page_size)
+  if (dtype == STAR_F32)
+    STAR_KVA(float);
+  else if (dtype == STAR_BF16)
+    STAR_KVA(__nv_bfloat16);
+  else
+    return fail(STAR_ECONFIG, "kv_append: unknown dtype %d", dtype);
+#undef STAR_KVA
+  STAR_LAUNCH_CHECK("kv_append");
+  return STAR_OK;
+}
+
 // ------------------------------------------------------------------ paged KV
 // Vector width W bytes; each thread moves one W-byte chunk of one (row, head).
 template <typename V>

@@ -376,11 +376,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   const int G = hq / hkv;
   const int QR = G * lq;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t len = kv_len[b];
   const int64_t r0 = (int64_t)split * chunk;
-  const int64_t r1 = min(len, r0 + chunk);
-  const int64_t tail0 = len - own_tail;
-  const int ntiles = r1 > r0 ? (int)((r1 - r0 + TN - 1) / TN) : 0;
   const int32_t* table = page_table + (int64_t)b * pages_per_seq;
   float* out_part = out + (int64_t)split * part_stride_rows * D;
   float* lse_part = lse + (int64_t)split * part_stride_rows;
@@ -393,7 +389,19 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
     }
     fence_mbar_init();
   }
+  if (warp == NC && lane == 0) {
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+  }
   __syncthreads();
+  // Launched as a programmatic dependent (PDL) of the kernel before it (e.g. the decode
+  // append that writes q's row and bumps kv_len): everything above overlapped that kernel;
+  // nothing it writes is read before this point.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t len = kv_len[b];
+  const int64_t r1 = min(len, r0 + chunk);
+  const int64_t tail0 = len - own_tail;
+  const int ntiles = r1 > r0 ? (int)((r1 - r0 + TN - 1) / TN) : 0;
 
   if (warp == NC) {
     // ================= TMA producer =================
@@ -401,10 +409,6 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
     // one coalesced load, the next group's load in flight while this group is issued);
     // lane 0 then issues the TMA loads back to back, so the ring fills without a
     // dependent table read in front of every tile.
-    if (lane == 0) {
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-    }
     // bounded by the split's chunk, not by kv_len: the first table load does not wait for
     // the kv_len load (tiles past the sequence end are resolved but never issued)
     const int tiles_cap = (int)(chunk / TN);
@@ -833,11 +837,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
   const int G = hq / hkv;
   const int QR = G * lq;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t len = kv_len[b];
   const int64_t r0 = (int64_t)split * chunk;
-  const int64_t r1 = min(len, r0 + chunk);
-  const int64_t tail0 = len - own_tail;
-  const int ntiles = r1 > r0 ? (int)((r1 - r0 + BN - 1) / BN) : 0;
   const int32_t* table = page_table + (int64_t)b * pages_per_seq;
   uint2* const w_lse = w_out + (int64_t)gridDim.x * part_rows * D;
 
@@ -859,6 +859,12 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  // programmatic dependent launch: the setup above overlapped the previous kernel
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t len = kv_len[b];
+  const int64_t r1 = min(len, r0 + chunk);
+  const int64_t tail0 = len - own_tail;
+  const int ntiles = r1 > r0 ? (int)((r1 - r0 + BN - 1) / BN) : 0;
 
   // pool row of the 64-key half `hh` of tile t (a half past the split end re-reads the
   // tile's first half, whose extra keys the softmax masks)
@@ -1125,6 +1131,18 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
 // ------------------------------------------------------------------ host
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 
+// K2 / K2q are launched as programmatic dependents of the kernel before them (their setup
+// overlaps it; griddepcontrol.wait precedes every read of its outputs).  STAR_K2_PDL=0 turns
+// it off (measurement).
+static bool k2_pdl() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("STAR_K2_PDL");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // K2q (tcgen05 query encode) takes 16 < G*l_q <= 128 packed rows at head_dim 128 over a pool
 // of 64-key-aligned pages; STAR_K2_QE=0 turns it off (measurement)
 bool phase2_qe_eligible(int qrows, int d, int page_size) {
@@ -1230,16 +1248,23 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     cudaError_t e = cudaFuncSetAttribute(phase2_qe_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, p2q::kSmem);
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 qe smem attr: %s", cudaGetErrorString(e));
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (grp_epoch != nullptr) {  // cooperative only for the word-mode fold
+      attr[na].id = cudaLaunchAttributeCooperative;
+      attr[na++].val.cooperative = 1;
+    }
+    if (k2_pdl()) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(p2q::kThreads);
     cfg.dynamicSmemBytes = p2q::kSmem;
     cfg.stream = s;
     cfg.attrs = attr;
-    cfg.numAttrs = grp_epoch != nullptr ? 1 : 0;  // cooperative only for the word-mode fold
+    cfg.numAttrs = na;
     e = cudaLaunchKernelEx(&cfg, phase2_qe_kernel, tq, tk, tv, lq, hq, hkv, table, pps, page_size,
                            kv_len, own_tail, chunk, reinterpret_cast<uint2*>(out), part_rows, sl2,
                            final_out, final_lse, grp_epoch, pp);
@@ -1256,16 +1281,23 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     const int bytes = Smem<DD>::kBytes;                                                         \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \
-    cudaLaunchAttribute attr[1];                                                                \
-    attr[0].id = cudaLaunchAttributeCooperative;                                                \
-    attr[0].val.cooperative = 1;                                                                \
+    cudaLaunchAttribute attr[2];                                                                \
+    int na = 0;                                                                                 \
+    if (grp_epoch != nullptr) {                                                                 \
+      attr[na].id = cudaLaunchAttributeCooperative;                                             \
+      attr[na++].val.cooperative = 1;                                                           \
+    }                                                                                           \
+    if (k2_pdl()) {                                                                             \
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;                         \
+      attr[na++].val.programmaticStreamSerializationAllowed = 1;                                \
+    }                                                                                           \
     cudaLaunchConfig_t cfg = {};                                                                \
     cfg.gridDim = grid;                                                                         \
     cfg.blockDim = dim3(Cons<KS>::kThreads);                                                    \
     cfg.dynamicSmemBytes = bytes;                                                               \
     cfg.stream = s;                                                                             \
     cfg.attrs = attr;                                                                           \
-    cfg.numAttrs = grp_epoch != nullptr ? 1 : 0;                                                \
+    cfg.numAttrs = na;                                                                          \
     e = cudaLaunchKernelEx(&cfg, kern, tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, pps, \
                            page_size, kv_len, own_tail, chunk, out, lse, part_rows, sl2,        \
                            final_out, final_lse, counters, grp_epoch, pp);                      \

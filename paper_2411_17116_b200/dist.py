@@ -86,6 +86,14 @@ def rank_shard(plan: BlockPlan, blocks_aug, rank: int) -> RankShard:
 def gather_packed(packed: torch.Tensor, group=None) -> torch.Tensor:
     """ONE all-gather of every rank's packed partial [rows*d out | rows lse] -> [world, rows*(d+1)]."""
     world = dist.get_world_size(group)
+    if packed.is_cuda and dist.get_backend(group) != "nccl":
+        # host-staged collective (gloo: the multi-rank test backend): an explicit device->host
+        # read and host->device write, so the result never depends on a CPU backend's handling
+        # of CUDA-stream ordering
+        host = packed.contiguous().view(-1).cpu()
+        parts = torch.empty(world * host.numel(), dtype=host.dtype)
+        dist.all_gather_into_tensor(parts, host, group=group)
+        return parts.to(packed.device).view(world, packed.numel())
     parts = torch.empty(world * packed.numel(), dtype=packed.dtype, device=packed.device)
     dist.all_gather_into_tensor(parts, packed.contiguous().view(-1), group=group)
     return parts.view(world, packed.numel())

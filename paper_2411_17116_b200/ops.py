@@ -117,6 +117,42 @@ def rope_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, positions: torch
     return q_out, k_out
 
 
+def kv_append(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, positions: torch.Tensor,
+              kv_len: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
+              page_table: torch.Tensor, theta: float = 10000.0,
+              q_out: torch.Tensor | None = None) -> torch.Tensor:
+    """Decode append (star_kv_append) for B = kv_len.numel() sequences of rows/B new rows each:
+    rotated q returned; rotated k / raw v written at the rows each sequence's device counter
+    kv_len[b] (int32) names, counters advanced — one launch, no host value, graph-capturable.
+    page_table: [B, pages_per_seq] (or [pages] for B = 1)."""
+    _cuda(q, k, v, positions, kv_len, k_pages, v_pages, page_table)
+    n, hq, qs = _rows_view(q, "q")
+    rk, hkv, ks = _rows_view(k, "k")
+    if rk != n or tuple(v.shape) != tuple(k.shape) or v.stride() != k.stride():
+        raise ShapeError("q/k/v rows or k/v layouts disagree")
+    if not (q.dtype == k.dtype == v.dtype == k_pages.dtype == v_pages.dtype):
+        raise ConfigError("q, k, v and the pools must share a dtype")
+    if positions.dtype != torch.int64 or positions.numel() != n:
+        raise ShapeError(f"{positions.numel()} positions for {n} rows (int64 required)")
+    if kv_len.dtype != torch.int32 or page_table.dtype != torch.int32:
+        raise ConfigError("kv_len and page_table must be int32")
+    B = kv_len.numel()
+    if B < 1 or n % B:
+        raise ShapeError(f"{n} rows do not split over {B} sequences")
+    pt = page_table.view(1, -1) if page_table.dim() == 1 else page_table
+    if pt.shape[0] != B or not pt.is_contiguous():
+        raise ShapeError("page_table must be a contiguous [batch, pages_per_seq] table")
+    if k_pages.dim() != 4 or k_pages.shape[1] != hkv or k_pages.shape[3] != q.shape[2]:
+        raise ShapeError("paged pool does not match k")
+    q_out = torch.empty_like(q) if q_out is None else q_out
+    _, _, qos = _rows_view(q_out, "q_out")
+    _lib.call("star_kv_append", q.data_ptr(), k.data_ptr(), v.data_ptr(), dtype_code(q), B, n // B,
+              hq, hkv, q.shape[2], qs, ks, q_out.data_ptr(), qos, positions.contiguous().data_ptr(),
+              float(theta), kv_len.data_ptr(), k_pages.data_ptr(), v_pages.data_ptr(),
+              pt.data_ptr(), pt.shape[1], k_pages.shape[2], _stream(q.device))
+    return q_out
+
+
 # ---------------------------------------------------------------------------- phase 1
 def phase1_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_start: Sequence[int],
                out: torch.Tensor | None = None, want_lse: bool = False, out_dtype=None,

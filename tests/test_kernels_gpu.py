@@ -411,3 +411,34 @@ def test_phase1_more_segments_than_one_launch(ops, dtype):
         dd, dd_l = ops.phase1_fwd(q, k, v, seg, want_lse=True, dedup_anchor_rows=a)
         torch.cuda.synchronize()
         assert torch.equal(full, dd) and torch.equal(full_l, dd_l)
+
+
+@pytest.mark.parametrize("dtype,B,rows", [(torch.bfloat16, 1, 1), (torch.float32, 1, 3),
+                                          (torch.bfloat16, 4, 1), (torch.bfloat16, 3, 2)])
+def test_kv_append_equals_rope_and_page_write(ops, dtype, B, rows):
+    """star_kv_append (the graph-safe decode append): rotated q, and rotated k / raw v at the
+    rows each sequence's DEVICE counter names, bit-exact against rope + kv_write at host rows;
+    counters advanced by `rows`."""
+    hq, hkv, d, page = 8, 2, 128, 64
+    pps = 3
+    n = B * rows
+    q = torch.randn(n, hq, d).to(dtype).cuda()
+    k = torch.randn(n, hkv, d).to(dtype).cuda()
+    v = torch.randn(n, hkv, d).to(dtype).cuda()
+    pos = torch.randint(0, 1 << 20, (n,), dtype=torch.int64).cuda()
+    start = [37, 63, 0, 120][:B]  # crosses a page boundary for sequence 1
+    kv_len = torch.tensor(start, dtype=torch.int32).cuda()
+    table = torch.randperm(B * pps).to(torch.int32).view(B, pps).cuda()
+    kp = torch.zeros((B * pps, hkv, page, d), dtype=dtype, device="cuda")
+    vp = torch.zeros_like(kp)
+    qo = ops.kv_append(q, k, v, pos, kv_len, kp, vp, table)
+    kp2, vp2 = torch.zeros_like(kp), torch.zeros_like(vp)
+    q_ref = ops.rope(q, pos)
+    k_ref = ops.rope(k, pos)
+    for b in range(B):
+        sl = slice(b * rows, (b + 1) * rows)
+        ops.kv_write(k_ref[sl], v[sl], kp2, vp2, table[b].contiguous(), start[b])
+    torch.cuda.synchronize()
+    assert torch.equal(qo, q_ref)
+    assert torch.equal(kp, kp2) and torch.equal(vp, vp2)
+    assert kv_len.tolist() == [s + rows for s in start]
