@@ -703,8 +703,9 @@ def decode_layers_step(dev, world, rank, own_rows, ex, k2_us, barrier, max_over_
     import torch.distributed as tdist
 
     group = tdist.group.WORLD if (world > 1 and ex is None) else None
+    table = ops.RopeTable(L, room, d, 10000.0, dev)  # cos/sin of the decode positions
     attend = paged_attend(pool, appends=rank == q_rank, max_rows=own_rows + room, theta=10000.0,
-                          heads=hq, exchange=ex, group=group)
+                          heads=hq, exchange=ex, group=group, rope_table=table)
     launches = [0]
 
     def step():
@@ -737,8 +738,8 @@ def decode_layers_step(dev, world, rank, own_rows, ex, k2_us, barrier, max_over_
            "k2_kernel_us_per_layer": k2_us, "overhead_over_k2": us / n_layers / k2_us - 1.0,
            "hbm_frac_per_layer": kv_bytes / (us / n_layers * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6532.9),
            "tokens_timed": tokens, "cached_rows_per_rank": own_rows,
-           "path": "decoding.paged_attend per layer (query rank: star_rope_qkv append at the "
-                   "device row counter; K2" + (" with the fused peer exchange" if ex is not None
+           "path": "decoding.paged_attend per layer (query rank: star_kv_append at the "
+                   "device row counter, RoPE from the decode-position table; K2" + (" with the fused peer exchange" if ex is not None
                                                  else "") + "), 32 layers in one CUDA graph per token"}
     del pool, g
     torch.cuda.empty_cache()
@@ -781,9 +782,11 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
             kv_len = torch.full((B,), rows, dtype=torch.int32, device=dev)
             ws = ops.Phase2Workspace()
             maxk = rows + n_tokens
+            rtab = ops.RopeTable(rows, n_tokens + 8, d, 10000.0, dev)
 
             def step():
-                qr = ops.kv_append(q.view(B, hq, d), kn, vn, pos, kv_len, kp, vp, table)
+                qr = ops.kv_append(q.view(B, hq, d), kn, vn, pos, kv_len, kp, vp, table,
+                                   table=rtab)
                 ops.phase2_partial(qr.view(B, 1, hq, d), kp, vp, table, kv_len, maxk, workspace=ws)
                 pos.add_(1)
 

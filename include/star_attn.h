@@ -97,7 +97,18 @@ int star_kv_append(const void* q_in, const void* k_in, const void* v_in, int dty
                    int rows, int hq, int hkv, int d, int64_t q_in_stride, int64_t kv_in_stride,
                    void* q_out, int64_t q_out_stride, const int64_t* positions, double theta,
                    int32_t* kv_len, void* k_pages, void* v_pages, const int32_t* page_table,
-                   int pages_per_seq, int page_size, void* stream);
+                   int pages_per_seq, int page_size, const double* rope_table_cs,
+                   int64_t table_pos0, int64_t table_positions, void* stream);
+
+/*
+ * RoPE cos/sin table for positions [pos0, pos0 + n_positions): cs[(p*d/2 + i)*2 + {0,1}] =
+ * {cos, sin} of (pos0 + p) * theta^(-2i/d), fp64, the same expression star_rope evaluates
+ * (ss/numerics.py:173-176), so star_kv_append through the table (rope_table_cs != NULL and
+ * the position inside [table_pos0, table_pos0 + table_positions)) is bit-identical to
+ * forming the angle in place.  A decoder builds it once for its token budget.
+ */
+int star_rope_table(double* cs, int64_t pos0, int64_t n_positions, int d, double theta,
+                    void* stream);
 
 /*
  * Phase 1 (K1): causal self-attention over one or more anchor-augmented

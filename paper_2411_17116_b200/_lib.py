@@ -30,7 +30,9 @@ SIGNATURES = {
                               c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "star_kv_append": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
                                c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_double,
-                               c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
+                               c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p,
+                               c_int64, c_int64, c_void_p]),
+    "star_rope_table": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_void_p]),
     "star_phase1_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, POINTER(c_int64),
                                 c_int, c_int, c_int, c_int64, c_int64, c_void_p, c_int, c_int64,
                                 c_void_p, c_int64, c_void_p]),

@@ -261,7 +261,7 @@ class PagedKVPool:
             self.positions.extend(pos[len(self.positions) - row0:])
 
     def append_rope(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
-                    positions: torch.Tensor, theta: float) -> torch.Tensor:
+                    positions: torch.Tensor, theta: float, table=None) -> torch.Tensor:
         """Graph-safe append of one step's rows (star_kv_append, one launch): RoPE of q and k
         at the device `positions`, rotated k and raw v written at the rows the device counter
         kv_len_dev[layer] names, counter advanced on the device.  Returns rotated q.
@@ -269,7 +269,7 @@ class PagedKVPool:
         dt = self.dtype
         return ops.kv_append(q.to(dt).contiguous(), k.to(dt).contiguous(), v.to(dt).contiguous(),
                              positions, self.kv_len_dev[layer:layer + 1], self.k[layer],
-                             self.v[layer], self.page_table, theta)
+                             self.v[layer], self.page_table, theta, table=table)
 
     def rows(self, layer: int) -> int:
         return self.layer_rows[layer]

@@ -50,7 +50,8 @@ int rope_qkv(const void*, const void*, const void*, int, int64_t, int, int, int,
              const int32_t*, int, cudaStream_t);
 int kv_append(const void*, const void*, const void*, int, int, int, int, int, int, int64_t,
               int64_t, void*, int64_t, const int64_t*, double, int32_t*, void*, void*,
-              const int32_t*, int, int, cudaStream_t);
+              const int32_t*, int, int, const void*, int64_t, int64_t, cudaStream_t);
+int rope_table(void*, int64_t, int64_t, int, double, cudaStream_t);
 int kv_read(const void*, const void*, int, const int32_t*, int, int64_t, int64_t, int, int, void*,
             void*, cudaStream_t);
 int attention_simt(const void*, const void*, const void*, int, SegTable&, int, int, int, int64_t,
@@ -120,12 +121,20 @@ int star_kv_append(const void* q_in, const void* k_in, const void* v_in, int dty
                    int rows, int hq, int hkv, int d, int64_t q_in_stride, int64_t kv_in_stride,
                    void* q_out, int64_t q_out_stride, const int64_t* positions, double theta,
                    int32_t* kv_len, void* k_pages, void* v_pages, const int32_t* page_table,
-                   int pages_per_seq, int page_size, void* stream) {
+                   int pages_per_seq, int page_size, const double* rope_table_cs,
+                   int64_t table_pos0, int64_t table_positions, void* stream) {
   int rc = check_heads(hq, hkv, d);
   if (rc) return rc;
   return kv_append(q_in, k_in, v_in, dtype, batch, rows, hq, hkv, d, q_in_stride, kv_in_stride,
                    q_out, q_out_stride, positions, theta, kv_len, k_pages, v_pages, page_table,
-                   pages_per_seq, page_size, (cudaStream_t)stream);
+                   pages_per_seq, page_size, rope_table_cs, table_pos0, table_positions,
+                   (cudaStream_t)stream);
+}
+
+int star_rope_table(double* cs, int64_t pos0, int64_t n_positions, int d, double theta,
+                    void* stream) {
+  if (cs == nullptr && n_positions > 0) return fail(STAR_ESHAPE, "rope_table: out is NULL");
+  return rope_table(cs, pos0, n_positions, d, theta, (cudaStream_t)stream);
 }
 
 int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int n_seg,

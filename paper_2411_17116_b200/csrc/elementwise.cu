@@ -3,6 +3,8 @@
 //   * adjacent-pair RoPE at explicit positions, fp64 angles (ss/numerics.py:161-180)
 //   * paged KV-cache write / read (own-row retention ss/sim.py:117-118, append
 //     ss/blocking.py:161-170)
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace star {
@@ -189,13 +191,41 @@ int rope_qkv(const void* qi, const void* ki, const void* vi, int dtype, int64_t 
 // before and bumped after a CTA barrier).  It triggers its programmatic dependents at entry:
 // the K2 launch that follows (PDL) sets up beside it and waits in griddepcontrol.wait for
 // this kernel's stores.
+// cos / sin table of the decode positions [pos0, pos0 + n): entry (p, i) = {cos, sin} of
+// (pos0 + p) * theta^(-2i/d), the same fp64 expression as rope_kernel / rope_qkv_kernel, so a
+// rotation through the table is bit-identical to one that forms the angle in place.  Built
+// once per decoder (outside the per-token graph); the per-token append then spends no fp64
+// pow / sincos latency.
+__global__ void rope_table_kernel(double2* __restrict__ cs, int64_t pos0, int64_t n, int d,
+                                  double theta) {
+  const int half = d >> 1;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n * half) return;
+  const int64_t p = idx / half;
+  const int i = (int)(idx - p * half);
+  double sn, c;
+  sincos((double)(pos0 + p) * pow(theta, -2.0 * (double)i / (double)d), &sn, &c);
+  cs[idx] = make_double2(c, sn);
+}
+
+int rope_table(void* cs, int64_t pos0, int64_t n, int d, double theta, cudaStream_t s) {
+  if (d < 2 || (d & 1)) return fail(STAR_ECONFIG, "rope head_dim must be even and >= 2, got %d", d);
+  if (!(theta > 0)) return fail(STAR_ECONFIG, "rope theta must be positive, got %g", theta);
+  if (n < 0 || pos0 < 0) return fail(STAR_ESHAPE, "rope_table: bad position range");
+  if (n == 0) return STAR_OK;
+  const int64_t m = n * (d / 2);
+  rope_table_kernel<<<(int)((m + 255) / 256), 256, 0, s>>>((double2*)cs, pos0, n, d, theta);
+  STAR_LAUNCH_CHECK("rope_table");
+  return STAR_OK;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) kv_append_kernel(
     const T* __restrict__ qi, const T* __restrict__ ki, const T* __restrict__ vi,
     T* __restrict__ qo, int rows, int hq, int hkv, int d, int64_t qis, int64_t kis, int64_t qos,
     const int64_t* __restrict__ pos, double theta, int32_t* __restrict__ kv_len,
     T* __restrict__ kp, T* __restrict__ vp, const int32_t* __restrict__ page_table, int pps,
-    int page_size) {
+    int page_size, const double2* __restrict__ rtab, int64_t rtab_pos0, int64_t rtab_n) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // no-op unless launched as a dependent
   const int b = blockIdx.x;
@@ -206,7 +236,14 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
     const int rl = idx / half, i = idx - rl * half;
     const int64_t r = (int64_t)b * rows + rl;  // row of the q/k/v inputs
     double sn, cs;
-    sincos((double)pos[r] * pow(theta, -2.0 * (double)i / (double)d), &sn, &cs);
+    const int64_t tp = pos[r] - rtab_pos0;
+    if (rtab != nullptr && tp >= 0 && tp < rtab_n) {
+      const double2 e = rtab[tp * half + i];
+      cs = e.x;
+      sn = e.y;
+    } else {
+      sincos((double)pos[r] * pow(theta, -2.0 * (double)i / (double)d), &sn, &cs);
+    }
     const T* q = qi + r * qis + 2 * i;
     T* qw = qo + r * qos + 2 * i;
     for (int h = 0; h < hq; ++h) {
@@ -237,7 +274,8 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
 int kv_append(const void* qi, const void* ki, const void* vi, int dtype, int batch, int rows,
               int hq, int hkv, int d, int64_t qis, int64_t kis, void* qo, int64_t qos,
               const int64_t* pos, double theta, int32_t* kv_len, void* kp, void* vp,
-              const int32_t* table, int pps, int page_size, cudaStream_t s) {
+              const int32_t* table, int pps, int page_size, const void* rtab, int64_t rtab_pos0,
+              int64_t rtab_n, cudaStream_t s) {
   if (d < 2 || (d & 1)) return fail(STAR_ECONFIG, "rope head_dim must be even and >= 2, got %d", d);
   if (!(theta > 0)) return fail(STAR_ECONFIG, "rope theta must be positive, got %g", theta);
   if (batch < 0 || rows < 0 || hq < 1 || hkv < 1 || page_size < 1 || pps < 1)
@@ -252,18 +290,38 @@ int kv_append(const void* qi, const void* ki, const void* vi, int dtype, int bat
   if (batch == 0 || rows == 0) return STAR_OK;
   // (the counters live on the device: the caller reserves pps * page_size rows per sequence
   // for the whole decode, DeviceDecoder / PagedKVPool.reserve)
-#define STAR_KVA(T)                                                                                \
-  kv_append_kernel<T><<<batch, 256, 0, s>>>((const T*)qi, (const T*)ki, (const T*)vi, (T*)qo,     \
-                                            rows, hq, hkv, d, qis, kis, qos, pos, theta, kv_len,   \
-                                            (T*)kp, (T*)vp, table, pps, page_size)
+  // launched as a programmatic dependent of the kernel before it (typically the previous
+  // layer's K2): its CTA becomes resident while that kernel drains and waits in
+  // griddepcontrol.wait (STAR_K2_PDL=0: plain launch)
+  static int pdl = -1;
+  if (pdl < 0) {
+    const char* e = getenv("STAR_K2_PDL");
+    pdl = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(batch);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl;
+  cudaError_t e;
   if (dtype == STAR_F32)
-    STAR_KVA(float);
+    e = cudaLaunchKernelEx(&cfg, kv_append_kernel<float>, (const float*)qi, (const float*)ki,
+                           (const float*)vi, (float*)qo, rows, hq, hkv, d, qis, kis, qos, pos,
+                           theta, kv_len, (float*)kp, (float*)vp, table, pps, page_size,
+                           (const double2*)rtab, rtab_pos0, rtab_n);
   else if (dtype == STAR_BF16)
-    STAR_KVA(__nv_bfloat16);
+    e = cudaLaunchKernelEx(&cfg, kv_append_kernel<__nv_bfloat16>, (const __nv_bfloat16*)qi,
+                           (const __nv_bfloat16*)ki, (const __nv_bfloat16*)vi, (__nv_bfloat16*)qo,
+                           rows, hq, hkv, d, qis, kis, qos, pos, theta, kv_len, (__nv_bfloat16*)kp,
+                           (__nv_bfloat16*)vp, table, pps, page_size, (const double2*)rtab,
+                           rtab_pos0, rtab_n);
   else
     return fail(STAR_ECONFIG, "kv_append: unknown dtype %d", dtype);
-#undef STAR_KVA
-  STAR_LAUNCH_CHECK("kv_append");
+  if (e != cudaSuccess) return fail(STAR_ECUDA, "kv_append launch: %s", cudaGetErrorString(e));
   return STAR_OK;
 }
 

@@ -99,7 +99,7 @@ class DeviceDecoder:
 
 
 def paged_attend(pool, *, appends: bool, max_rows: int, theta: float, heads: int,
-                 exchange=None, group=None) -> AttendLayer:
+                 exchange=None, group=None, rope_table=None) -> AttendLayer:
     """Graph-safe phase-2 attention of one decode token against this rank's paged cache
     `pool` (the DeviceDecoder `attend_layer` of one rank; also the bench's 32-layer step).
 
@@ -110,6 +110,8 @@ def paged_attend(pool, *, appends: bool, max_rows: int, theta: float, heads: int
     rank's box and merges every rank's partial (C1 fused); None with a process group: K2 +
     one all-gather of the packed partial + K3; None without a group: K2 alone (one host).
     A rank with no rows pushes an empty partial (lse = -inf) so the merge stays collective.
+    rope_table: ops.RopeTable of the decode positions (the append then reads cos/sin instead
+    of forming fp64 angles per token; bit-identical).
     Returns the merged attention [1, H, hd] (fp32)."""
     H, hd = heads, pool.head_dim
     hkv = pool.hkv
@@ -117,7 +119,7 @@ def paged_attend(pool, *, appends: bool, max_rows: int, theta: float, heads: int
 
     def attend(li, q, k, v, pos):
         if appends:
-            qr = pool.append_rope(li, q, k, v, pos, theta)
+            qr = pool.append_rope(li, q, k, v, pos, theta, table=rope_table)
         else:
             qr = ops.rope(q.to(pool.dtype).contiguous(), pos, theta)
         qb = qr.view(1, 1, H, hd)

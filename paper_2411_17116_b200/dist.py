@@ -420,6 +420,7 @@ def decode_dist(sess: DistSession, n_tokens: int, group=None, graph: bool | None
     when the transport allows it (the peer exchange, or NCCL collectives; a gloo group runs
     the same device step eagerly).  No collective or host sync per token: the ids are read
     back once per call."""
+    from . import ops
     from .decoding import DeviceDecoder, paged_attend
 
     if n_tokens <= 0:
@@ -437,10 +438,14 @@ def decode_dist(sess: DistSession, n_tokens: int, group=None, graph: bool | None
             sess.pool.reserve(rows + room, exact=True)
         # every rank sizes its decoder for the same token budget
         budget = -(-max(n_tokens, 64) // 64) * 64
+        # (paged_attend's group=None means one host: pass the process group explicitly)
+        table = (ops.RopeTable(sess.next_position, room, cfg.head_dim, cfg.rope_theta,
+                               sess.pool.device) if room else None)
         attend = paged_attend(sess.pool, appends=rank == sess.q_rank,
                               max_rows=rows + room if rank in sess.nonempty else 0,
                               theta=cfg.rope_theta, heads=cfg.heads, exchange=sess.exchange,
-                              group=group)
+                              group=group if group is not None else dist.group.WORLD,
+                              rope_table=table)
         dec = DeviceDecoder(sess.weights, sess.last_logits, sess.next_position, attend, budget,
                             graph)
         sess._decoder = dec

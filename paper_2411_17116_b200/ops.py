@@ -117,14 +117,25 @@ def rope_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, positions: torch
     return q_out, k_out
 
 
+class RopeTable:
+    """cos/sin of the decode positions [pos0, pos0 + n) (star_rope_table), fp64 [n, d/2, 2]."""
+
+    def __init__(self, pos0: int, n: int, d: int, theta: float, device):
+        self.pos0, self.n, self.d, self.theta = int(pos0), int(n), int(d), float(theta)
+        self.cs = torch.empty((max(self.n, 1), d // 2, 2), dtype=torch.float64, device=device)
+        _lib.call("star_rope_table", self.cs.data_ptr(), self.pos0, self.n, self.d, self.theta,
+                  _stream(self.cs.device))
+
+
 def kv_append(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, positions: torch.Tensor,
               kv_len: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
               page_table: torch.Tensor, theta: float = 10000.0,
-              q_out: torch.Tensor | None = None) -> torch.Tensor:
+              q_out: torch.Tensor | None = None, table: RopeTable | None = None) -> torch.Tensor:
     """Decode append (star_kv_append) for B = kv_len.numel() sequences of rows/B new rows each:
     rotated q returned; rotated k / raw v written at the rows each sequence's device counter
     kv_len[b] (int32) names, counters advanced — one launch, no host value, graph-capturable.
-    page_table: [B, pages_per_seq] (or [pages] for B = 1)."""
+    page_table: [B, pages_per_seq] (or [pages] for B = 1).  table: precomputed cos/sin of the
+    decode positions (bit-identical; positions outside it form the angle in place)."""
     _cuda(q, k, v, positions, kv_len, k_pages, v_pages, page_table)
     n, hq, qs = _rows_view(q, "q")
     rk, hkv, ks = _rows_view(k, "k")
@@ -144,12 +155,17 @@ def kv_append(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, positions: torc
         raise ShapeError("page_table must be a contiguous [batch, pages_per_seq] table")
     if k_pages.dim() != 4 or k_pages.shape[1] != hkv or k_pages.shape[3] != q.shape[2]:
         raise ShapeError("paged pool does not match k")
+    if table is not None and (table.d != q.shape[2] or table.theta != float(theta)):
+        raise ConfigError("rope table was built for another head_dim / theta")
     q_out = torch.empty_like(q) if q_out is None else q_out
     _, _, qos = _rows_view(q_out, "q_out")
     _lib.call("star_kv_append", q.data_ptr(), k.data_ptr(), v.data_ptr(), dtype_code(q), B, n // B,
               hq, hkv, q.shape[2], qs, ks, q_out.data_ptr(), qos, positions.contiguous().data_ptr(),
               float(theta), kv_len.data_ptr(), k_pages.data_ptr(), v_pages.data_ptr(),
-              pt.data_ptr(), pt.shape[1], k_pages.shape[2], _stream(q.device))
+              pt.data_ptr(), pt.shape[1], k_pages.shape[2],
+              table.cs.data_ptr() if table is not None else None,
+              table.pos0 if table is not None else 0, table.n if table is not None else 0,
+              _stream(q.device))
     return q_out
 
 

@@ -322,13 +322,13 @@ def forward_star(weights: ModelWeights, tokens, plan: BlockPlan, spec: AnchorSpe
     return logits
 
 
-def _device_attend(hosts, qh: Host, max_rows: dict, theta: float):
+def _device_attend(hosts, qh: Host, max_rows: dict, theta: float, table=None):
     """Graph-safe phase-2 attention of one decode token (DeviceDecoder.attend_layer): append to
     the query host on the device, K2 on every non-empty host's pages with the device row
     counts, merge in ascending host order (ss/sim.py:254-281, :178-213)."""
 
     def attend(li, q, k, v, pos):
-        qr = qh.pool.append_rope(li, q, k, v, pos, theta)
+        qr = qh.pool.append_rope(li, q, k, v, pos, theta, table=table)
         H, hd = qr.shape[1], qr.shape[2]
         q4 = qr.view(1, 1, H, hd)
         parts = []
@@ -370,8 +370,11 @@ def decode(session: DecodeSession, n_tokens: int, greedy: bool = True,
         qh.pool.reserve(rows + room, exact=True)
         max_rows = {h.index: h.pool.rows(0) for h in hosts}
         max_rows[qh.index] = rows + room
+        table = ops.RopeTable(session.next_position, room, cfg.head_dim, cfg.rope_theta,
+                              qh.pool.device)
         dec = DeviceDecoder(session.weights, session.last_logits, session.next_position,
-                            _device_attend(hosts, qh, max_rows, cfg.rope_theta), room, graph)
+                            _device_attend(hosts, qh, max_rows, cfg.rope_theta, table), room,
+                            graph)
         session._decoder = dec
     new_tokens = dec.run(n_tokens)
     # host mirror of what the device step did

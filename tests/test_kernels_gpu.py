@@ -425,13 +425,18 @@ def test_kv_append_equals_rope_and_page_write(ops, dtype, B, rows):
     q = torch.randn(n, hq, d).to(dtype).cuda()
     k = torch.randn(n, hkv, d).to(dtype).cuda()
     v = torch.randn(n, hkv, d).to(dtype).cuda()
-    pos = torch.randint(0, 1 << 20, (n,), dtype=torch.int64).cuda()
+    pos = torch.randint(1000, 1200, (n,), dtype=torch.int64).cuda()
     start = [37, 63, 0, 120][:B]  # crosses a page boundary for sequence 1
     kv_len = torch.tensor(start, dtype=torch.int32).cuda()
     table = torch.randperm(B * pps).to(torch.int32).view(B, pps).cuda()
     kp = torch.zeros((B * pps, hkv, page, d), dtype=dtype, device="cuda")
     vp = torch.zeros_like(kp)
     qo = ops.kv_append(q, k, v, pos, kv_len, kp, vp, table)
+    # through a cos/sin table of (some of) the positions: bit-identical
+    kv_len_t = torch.tensor(start, dtype=torch.int32).cuda()
+    kp_t, vp_t = torch.zeros_like(kp), torch.zeros_like(vp)
+    tab = ops.RopeTable(1000, 100, d, 10000.0, "cuda")  # positions >= 1100 form angles in place
+    qo_t = ops.kv_append(q, k, v, pos, kv_len_t, kp_t, vp_t, table, table=tab)
     kp2, vp2 = torch.zeros_like(kp), torch.zeros_like(vp)
     q_ref = ops.rope(q, pos)
     k_ref = ops.rope(k, pos)
@@ -439,6 +444,7 @@ def test_kv_append_equals_rope_and_page_write(ops, dtype, B, rows):
         sl = slice(b * rows, (b + 1) * rows)
         ops.kv_write(k_ref[sl], v[sl], kp2, vp2, table[b].contiguous(), start[b])
     torch.cuda.synchronize()
-    assert torch.equal(qo, q_ref)
+    assert torch.equal(qo, q_ref) and torch.equal(qo_t, q_ref)
     assert torch.equal(kp, kp2) and torch.equal(vp, vp2)
-    assert kv_len.tolist() == [s + rows for s in start]
+    assert torch.equal(kp_t, kp2) and torch.equal(vp_t, vp2)
+    assert kv_len.tolist() == [s + rows for s in start] == kv_len_t.tolist()
