@@ -220,12 +220,48 @@ int rope_table(void* cs, int64_t pos0, int64_t n, int d, double theta, cudaStrea
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) kv_append_kernel(
+struct Pair;  // two adjacent elements moved as one load / store
+template <>
+struct Pair<float> {
+  using V = float2;
+  static __device__ __forceinline__ void get(V v, double& a, double& b) { a = v.x; b = v.y; }
+  static __device__ __forceinline__ V make(double a, double b) {
+    return make_float2(__double2float_rn(a), __double2float_rn(b));
+  }
+};
+template <>
+struct Pair<__nv_bfloat16> {
+  using V = __nv_bfloat162;
+  static __device__ __forceinline__ void get(V v, double& a, double& b) {
+    a = __bfloat162float(v.x);
+    b = __bfloat162float(v.y);
+  }
+  static __device__ __forceinline__ V make(double a, double b) {
+    V r;
+    r.x = __float2bfloat16_rn(__double2float_rn(a));
+    r.y = __float2bfloat16_rn(__double2float_rn(b));
+    return r;
+  }
+};
+
+constexpr int kAppendThreads = 512;
+constexpr int kAppendUnroll = 4;
+
+// One CTA per sequence.  Phase A: the (row, pair) cos/sin of the new rows into shared memory
+// (from the decode-position table, else formed in place).  Phase B: every (row, head, pair)
+// of q and k rotated and every (row, head, pair) of v copied — one independent 2-element item
+// per thread, kAppendUnroll items in flight per thread (all loads issued before any store),
+// so the kernel costs about one memory round trip instead of one per head.
+template <typename T>
+__global__ void __launch_bounds__(kAppendThreads) kv_append_kernel(
     const T* __restrict__ qi, const T* __restrict__ ki, const T* __restrict__ vi,
     T* __restrict__ qo, int rows, int hq, int hkv, int d, int64_t qis, int64_t kis, int64_t qos,
     const int64_t* __restrict__ pos, double theta, int32_t* __restrict__ kv_len,
     T* __restrict__ kp, T* __restrict__ vp, const int32_t* __restrict__ page_table, int pps,
     int page_size, const double2* __restrict__ rtab, int64_t rtab_pos0, int64_t rtab_n) {
+  using P = Pair<T>;
+  using V = typename P::V;
+  extern __shared__ double2 cs_s[];  // [rows][half]
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // no-op unless launched as a dependent
   const int b = blockIdx.x;
@@ -234,37 +270,64 @@ __global__ void __launch_bounds__(256) kv_append_kernel(
   const int32_t* table = page_table + (int64_t)b * pps;
   for (int idx = threadIdx.x; idx < rows * half; idx += blockDim.x) {
     const int rl = idx / half, i = idx - rl * half;
-    const int64_t r = (int64_t)b * rows + rl;  // row of the q/k/v inputs
-    double sn, cs;
-    const int64_t tp = pos[r] - rtab_pos0;
+    const int64_t p = pos[(int64_t)b * rows + rl];
+    const int64_t tp = p - rtab_pos0;
     if (rtab != nullptr && tp >= 0 && tp < rtab_n) {
-      const double2 e = rtab[tp * half + i];
-      cs = e.x;
-      sn = e.y;
+      cs_s[idx] = rtab[tp * half + i];
     } else {
-      sincos((double)pos[r] * pow(theta, -2.0 * (double)i / (double)d), &sn, &cs);
+      double sn, c;
+      sincos((double)p * pow(theta, -2.0 * (double)i / (double)d), &sn, &c);
+      cs_s[idx] = make_double2(c, sn);
     }
-    const T* q = qi + r * qis + 2 * i;
-    T* qw = qo + r * qos + 2 * i;
-    for (int h = 0; h < hq; ++h) {
-      const double x0 = Elem<T>::to_f(q[h * d]), x1 = Elem<T>::to_f(q[h * d + 1]);
-      qw[h * d] = Elem<T>::from_f(__double2float_rn(x0 * cs - x1 * sn));
-      qw[h * d + 1] = Elem<T>::from_f(__double2float_rn(x0 * sn + x1 * cs));
+  }
+  __syncthreads();
+  const int nq = rows * hq * half, nk = rows * hkv * half;
+  const int total = nq + 2 * nk;
+  for (int i0 = threadIdx.x; i0 < total; i0 += kAppendUnroll * kAppendThreads) {
+    V val[kAppendUnroll];
+#pragma unroll
+    for (int u = 0; u < kAppendUnroll; ++u) {
+      const int idx = i0 + u * kAppendThreads;
+      if (idx >= total) break;
+      const T* src;
+      if (idx < nq) {
+        const int rl = idx / (hq * half), rem = idx - rl * hq * half;
+        src = qi + ((int64_t)b * rows + rl) * qis + 2 * rem;
+      } else {
+        const int j = idx < nq + nk ? idx - nq : idx - nq - nk;
+        const int rl = j / (hkv * half), rem = j - rl * hkv * half;
+        src = (idx < nq + nk ? ki : vi) + ((int64_t)b * rows + rl) * kis + 2 * rem;
+      }
+      val[u] = *reinterpret_cast<const V*>(src);
     }
-    const int64_t cr = base + rl;
-    const int64_t page = table[cr / page_size];
-    const int64_t slot = cr % page_size;
-    T* kpr = kp + (page * hkv * page_size + slot) * d + 2 * i;
-    T* vpr = vp + (page * hkv * page_size + slot) * d + 2 * i;
-    const T* k = ki + r * kis + 2 * i;
-    const T* v = vi + r * kis + 2 * i;
-    for (int h = 0; h < hkv; ++h) {
-      const double x0 = Elem<T>::to_f(k[h * d]), x1 = Elem<T>::to_f(k[h * d + 1]);
-      const int64_t po = (int64_t)h * page_size * d;
-      kpr[po] = Elem<T>::from_f(__double2float_rn(x0 * cs - x1 * sn));
-      kpr[po + 1] = Elem<T>::from_f(__double2float_rn(x0 * sn + x1 * cs));
-      vpr[po] = v[h * d];
-      vpr[po + 1] = v[h * d + 1];
+#pragma unroll
+    for (int u = 0; u < kAppendUnroll; ++u) {
+      const int idx = i0 + u * kAppendThreads;
+      if (idx >= total) break;
+      if (idx < nq) {
+        const int rl = idx / (hq * half), rem = idx - rl * hq * half;
+        const double2 e = cs_s[rl * half + rem % half];
+        double x0, x1;
+        P::get(val[u], x0, x1);
+        *reinterpret_cast<V*>(qo + ((int64_t)b * rows + rl) * qos + 2 * rem) =
+            P::make(x0 * e.x - x1 * e.y, x0 * e.y + x1 * e.x);
+      } else {
+        const bool is_k = idx < nq + nk;
+        const int j = is_k ? idx - nq : idx - nq - nk;
+        const int rl = j / (hkv * half), rem = j - rl * hkv * half;
+        const int h = rem / half, i = rem - h * half;
+        const int64_t cr = base + rl;
+        const int64_t page = table[cr / page_size];
+        const int64_t off = ((page * hkv + h) * page_size + cr % page_size) * d + 2 * i;
+        V outv = val[u];
+        if (is_k) {
+          const double2 e = cs_s[rl * half + i];
+          double x0, x1;
+          P::get(val[u], x0, x1);
+          outv = P::make(x0 * e.x - x1 * e.y, x0 * e.y + x1 * e.x);
+        }
+        *reinterpret_cast<V*>((is_k ? kp : vp) + off) = outv;
+      }
     }
   }
   __syncthreads();
@@ -301,9 +364,13 @@ int kv_append(const void* qi, const void* ki, const void* vi, int dtype, int bat
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  if ((int64_t)rows * (d / 2) * 16 > 48 * 1024)
+    return fail(STAR_ENOTSUP, "kv_append: %d rows per sequence exceed the cos/sin staging", rows);
+  if ((qis | kis | qos) & 1) return fail(STAR_ECONFIG, "kv_append: odd row strides");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(batch);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(kAppendThreads);
+  cfg.dynamicSmemBytes = (size_t)rows * (d / 2) * sizeof(double2);
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = pdl;

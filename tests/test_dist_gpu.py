@@ -84,6 +84,7 @@ def _worker(rank, port, name, q, transport, world, dtype="float32", backend="glo
                 f"{a},{b},{c},{k},{n}\n" for a, b, c, k, n in sess.ledger)
         q.put((rank, {"gen": gen, "ref": [int(t) for t in g["generated"]], "err": err, "csv": csv,
                       "sim": sim, "transport": transport_used,
+                      "last": sess.last_logits.float().cpu().numpy(),
                       "ref_csv": str(g["ledger_csv"]),
                       "pos": list(sess.pool.positions),
                       "ref_pos": [int(p) for p in g[f"host{rank}_pos_ch0"]]}))
@@ -125,6 +126,8 @@ def test_dist_session_ranks(name, transport, dtype, backend):
         assert "error" not in res, res
         assert res["pos"] == res["ref_pos"]
         assert res["transport"] == transport, res["transport"]  # no silent fallback
+        # every rank merges every partial: bit-identical logits on all ranks
+        assert np.array_equal(res["last"], out[0]["last"]), r
         if dtype == "float32":
             assert res["gen"] == res["ref"]
             assert res["err"] < 1e-4
