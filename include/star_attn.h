@@ -131,6 +131,17 @@ int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int 
                     int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
                     float* lse, int64_t dedup_anchor_rows, void* stream);
 
+/*
+ * Check mode of star_phase1_fwd (same arguments, no dedup): every dtype runs the CUDA-core
+ * kernel with fp32 scores, softmax and accumulation (ss/attention.py:109-122 at the
+ * reference's default fp32 precision) — the yardstick the bf16 tensor-core K1 is compared
+ * against, row for row, at full size (tests/test_fullsize_gpu.py).
+ */
+int star_phase1_fwd_check(const void* q, const void* k, const void* v, int dtype, int n_seg,
+                          const int64_t* seg_start, int hq, int hkv, int d,
+                          int64_t q_row_stride, int64_t kv_row_stride, void* out, int out_dtype,
+                          int64_t out_row_stride, float* lse, void* stream);
+
 /* Phase 1 over a query-row range of ONE segment: causal attention of query rows
  * [q_begin, q_end) against keys [0, q_end) of the segment whose row 0 is at q/k/v/out.
  * Equals causal_attention(q[q_begin:q_end], k[:q_end], v[:q_end], q_offset=q_begin)

@@ -36,6 +36,9 @@ SIGNATURES = {
     "star_phase1_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, POINTER(c_int64),
                                 c_int, c_int, c_int, c_int64, c_int64, c_void_p, c_int, c_int64,
                                 c_void_p, c_int64, c_void_p]),
+    "star_phase1_fwd_check": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, POINTER(c_int64),
+                                      c_int, c_int, c_int, c_int64, c_int64, c_void_p, c_int,
+                                      c_int64, c_void_p, c_void_p]),
     "star_phase1_fwd_range": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64,
                                       c_int, c_int, c_int, c_int64, c_int64, c_void_p, c_int,
                                       c_int64, c_void_p, c_int64, c_void_p]),

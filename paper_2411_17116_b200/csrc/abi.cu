@@ -137,10 +137,10 @@ int star_rope_table(double* cs, int64_t pos0, int64_t n_positions, int d, double
   return rope_table(cs, pos0, n_positions, d, theta, (cudaStream_t)stream);
 }
 
-int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int n_seg,
-                    const int64_t* seg_start, int hq, int hkv, int d, int64_t q_row_stride,
-                    int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
-                    float* lse, int64_t dedup_anchor_rows, void* stream) {
+static int phase1_impl(const void* q, const void* k, const void* v, int dtype, int n_seg,
+                       const int64_t* seg_start, int hq, int hkv, int d, int64_t q_row_stride,
+                       int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
+                       float* lse, int64_t dedup_anchor_rows, bool check_mode, void* stream) {
   int rc = check_heads(hq, hkv, d);
   if (out_dtype != STAR_F32 && out_dtype != STAR_BF16)
     return fail(STAR_ECONFIG, "phase1: unknown out dtype %d", out_dtype);
@@ -165,7 +165,7 @@ int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int 
   const int64_t total = seg_start[n_seg];
   const int64_t lse_stride = total;
   cudaStream_t s = (cudaStream_t)stream;
-  const bool tc = dtype == STAR_BF16 && (d == 64 || d == 128);
+  const bool tc = !check_mode && dtype == STAR_BF16 && (d == 64 || d == 128);
   if (tc && total >= (1ll << 31)) return fail(STAR_ENOTSUP, "phase1: more than 2^31 rows per call");
   // The segment table travels in the kernel parameter block (kMaxSegments entries), so a
   // context with more blocks runs as several stream-ordered launches of up to kMaxSegments
@@ -196,6 +196,22 @@ int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int 
     if (rc) return rc;
   }
   return STAR_OK;
+}
+
+int star_phase1_fwd(const void* q, const void* k, const void* v, int dtype, int n_seg,
+                    const int64_t* seg_start, int hq, int hkv, int d, int64_t q_row_stride,
+                    int64_t kv_row_stride, void* out, int out_dtype, int64_t out_row_stride,
+                    float* lse, int64_t dedup_anchor_rows, void* stream) {
+  return phase1_impl(q, k, v, dtype, n_seg, seg_start, hq, hkv, d, q_row_stride, kv_row_stride,
+                     out, out_dtype, out_row_stride, lse, dedup_anchor_rows, false, stream);
+}
+
+int star_phase1_fwd_check(const void* q, const void* k, const void* v, int dtype, int n_seg,
+                          const int64_t* seg_start, int hq, int hkv, int d,
+                          int64_t q_row_stride, int64_t kv_row_stride, void* out, int out_dtype,
+                          int64_t out_row_stride, float* lse, void* stream) {
+  return phase1_impl(q, k, v, dtype, n_seg, seg_start, hq, hkv, d, q_row_stride, kv_row_stride,
+                     out, out_dtype, out_row_stride, lse, 0, true, stream);
 }
 
 int star_phase1_fwd_range(const void* q, const void* k, const void* v, int dtype, int64_t q_begin,

@@ -228,6 +228,27 @@ def phase1_fwd_range(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_begin:
     return out
 
 
+def phase1_fwd_check(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_start: Sequence[int],
+                     out_dtype=torch.float32, want_lse: bool = True):
+    """Check mode of phase1_fwd: the fp32 CUDA-core kernel for any input dtype."""
+    _cuda(q, k, v)
+    rq, hq, qs = _rows_view(q, "q")
+    rk, hkv, ks = _rows_view(k, "k")
+    if tuple(v.shape) != tuple(k.shape) or v.stride() != k.stride():
+        raise ShapeError("k and v must share shape and row stride")
+    d = q.shape[2]
+    seg = [int(x) for x in seg_start]
+    if seg[-1] > rq or seg[-1] > rk:
+        raise ShapeError("segments extend past the q/k rows")
+    out = torch.empty((rq, hq, d), dtype=out_dtype, device=q.device)
+    lse = torch.empty((hq, seg[-1]), dtype=torch.float32, device=q.device) if want_lse else None
+    arr = (ctypes.c_int64 * len(seg))(*seg)
+    _lib.call("star_phase1_fwd_check", q.data_ptr(), k.data_ptr(), v.data_ptr(), dtype_code(q),
+              len(seg) - 1, arr, hq, hkv, d, qs, ks, out.data_ptr(), dtype_code(out), hq * d,
+              _ptr(lse), _stream(q.device))
+    return out, lse
+
+
 def attention_dense(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_offset: int = 0,
                     mask: str = "causal", want_lse: bool = True):
     """Masked attention of q [lq, hq, d] vs k/v [lk, hkv, d]; mask "causal" | "full"."""
