@@ -167,7 +167,7 @@ static bool pdl_enabled() {  // STAR_EXCHANGE_PDL=0 turns the early launch off (
   return v == 1;
 }
 
-static uint64_t exchange_timeout_ns() {
+uint64_t spin_timeout_ns() {
   static uint64_t t = 0;
   if (t == 0) {
     const char* e = getenv("STAR_EXCHANGE_TIMEOUT_S");
@@ -198,7 +198,7 @@ int exchange_merge(void* box, const ExchangeLayout& L, int batch, int lq, int hq
   if (rc) return rc;
   if (d > 128) return fail(STAR_ENOTSUP, "exchange: head_dim %d > 128", d);
   const int grid = (int)((nrows + kXWarps - 1) / kXWarps);
-  const uint64_t to = exchange_timeout_ns();
+  const uint64_t to = spin_timeout_ns();
   // Programmatic dependent launch: K3x may start while the producer kernel (K2 / push) is
   // still running — it needs none of its results beyond the epoch words it polls — so its
   // launch latency hides under K2 (K2 triggers at entry).  The header epoch it reads was

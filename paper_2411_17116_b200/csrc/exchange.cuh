@@ -67,7 +67,14 @@ struct PeerPush {
   // 1: the producer also merges every rank's partial of its slice (the whole exchange in
   // one kernel; only for a co-resident grid, see split_merge_words); 0: K3x merges
   int merge;
+  // spin-wait bound of the word protocols (split fold and peer merge) before __trap: a
+  // missing producer fails loudly instead of hanging the stream (STAR_EXCHANGE_TIMEOUT_S,
+  // default 30 s; raise it under compute-sanitizer, which slows every CTA down)
+  uint64_t timeout_ns;
 };
+
+// STAR_EXCHANGE_TIMEOUT_S (seconds, default 30), read once per process
+uint64_t spin_timeout_ns();
 
 __device__ __forceinline__ void st_word(uint2* p, float v, uint32_t e) {
   asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)),

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
       for (int i = 0; i < NQ; ++i) issue_s(i, 0);
-      umma_commit_warp(&k_empty[0]);
+      if (C::KST < nkv) umma_commit_warp(&k_empty[0]);
       for (int j = 0; j < nkv; ++j) {
         const int vs = j % C::VST;
         mbar_wait(&v_full[vs], (j / C::VST) & 1);
@@ -220,12 +220,14 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
             umma_bf16_ts_warp(tbase + NQ * C::BN + i * D, tbase + i * C::BN + kk * 8, bd, idesc_o,
                          (j > 0 || kk > 0) ? 1u : 0u);
           }
-          umma_commit_warp(&o_done[i]);
+          if (!next) umma_commit_warp(&o_done[i]);  // the epilogue's wait: the last P.V only
           if (next) issue_s(i, ks);
           K1_TR(bx == 0 && j < 256, 2 * 256 * 5 + (j * 2 + i) * 2 + 1);
         }
-        umma_commit_warp(&v_empty[vs]);
-        if (next) umma_commit_warp(&k_empty[ks]);
+        // release a stage only if the producer will refill it (a commit nobody waits for
+        // could still be in flight when the CTA exits)
+        if (j + C::VST < nkv) umma_commit_warp(&v_empty[vs]);
+        if (next && j + 1 + C::KST < nkv) umma_commit_warp(&k_empty[ks]);
       }
     }
   } else {
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       K1_TR(tr, (i * 256 + j) * 5 + 4);
     }
     // ---- epilogue: O / l -> rows; lse = ln(sum) + max ----
-    mbar_wait(&o_done[i], (nkv - 1) & 1);
+    mbar_wait(&o_done[i], 0);  // one phase: the commit after the last P.V
     tc_fence_after();
     const float inv = 1.f / l_run;
     const bool row_ok = qrow < lq && prm.out != nullptr;

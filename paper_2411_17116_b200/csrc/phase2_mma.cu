@@ -228,7 +228,7 @@ __device__ void exchange_merge_slice(int b, int kvh, int r_lo, int lq, int hq, i
       }
       if (all) break;
       if (t0 == 0) t0 = globaltimer_ns();
-      if (globaltimer_ns() - t0 > 30000000000ull) __trap();  // a peer never delivered
+      if (globaltimer_ns() - t0 > pp.timeout_ns) __trap();  // a peer never delivered
     }
     K2_TR(e == lo, 6);
     double mx = -INFINITY;
@@ -314,7 +314,7 @@ __device__ void split_merge_words(int b, int kvh, int r_lo, int r_n, int lq, int
         }
         if (all) break;
         if (t0 == 0) t0 = globaltimer_ns();
-        if (globaltimer_ns() - t0 > 20000000000ull) __trap();  // a split never landed
+        if (globaltimer_ns() - t0 > pp.timeout_ns) __trap();  // a split never landed
       }
       K2_TR(e == lo && p0 == 0, 4);
       float mn = m;
@@ -1161,6 +1161,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
                int* merged, cudaStream_t s) {
   using namespace p2;
   if (merged != nullptr) *merged = 0;
+  pp.timeout_ns = spin_timeout_ns();
   auto fn = tensor_map_encoder();
   if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if (page_size % TN) return fail(STAR_ECONFIG, "page_size must be a multiple of %d", TN);

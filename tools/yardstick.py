@@ -52,6 +52,22 @@ def main():
     res = {"rows": m, "heads_q": hq, "heads_kv": hkv, "head_dim": d, "flops": flops, "kernels": {}}
     ref = torch.empty_like(q)
     ops.phase1_fwd(q, k, v, [0, m], out=ref)
+    # accuracy yardstick: the fp32 CUDA-core check kernel on the same bf16 inputs
+    chk, _ = ops.phase1_fwd_check(q, k, v, [0, m], want_lse=False)
+
+    def accuracy(o):
+        """normwise error per (128-row block, head) vs the fp32 check kernel: max, p99.9,
+        share of blocks above 2e-3; and the worst per-head Frobenius relative error."""
+        o = o.float()
+        nb = m // 128
+        num = (o[:nb * 128] - chk[:nb * 128]).abs().view(nb, 128, hq, d).amax(dim=(1, 3))
+        den = chk[:nb * 128].abs().view(nb, 128, hq, d).amax(dim=(1, 3))
+        e = (num / den).flatten()
+        fro = ((o - chk).pow(2).sum(dim=(0, 2)).sqrt() / chk.pow(2).sum(dim=(0, 2)).sqrt()).max()
+        return {"block_normwise_max": float(e.max()),
+                "block_normwise_p999": float(e.quantile(0.999)),
+                "share_blocks_over_2e-3": float((e > 2e-3).float().mean()),
+                "frobenius_rel_max_head": float(fro)}
 
     def record(name, fn, check=None):
         t0 = time.time()
@@ -59,19 +75,25 @@ def main():
             out = fn()
             torch.cuda.synchronize()
             err = None
+            acc = None
             if check is not None:
                 o = check(out)
                 err = float((o.float() - ref.float()).abs().max() / ref.float().abs().max())
+                acc = accuracy(o)
             ms = timed(fn)
             res["kernels"][name] = {"ms": ms, "tflops": flops / (ms * 1e-3) / 1e12,
-                                    "normwise_vs_ours": err, "setup_s": time.time() - t0}
+                                    "normwise_vs_ours": err, "accuracy_vs_fp32": acc,
+                                    "setup_s": time.time() - t0}
         except Exception as exc:  # noqa: BLE001 - a yardstick that does not run is reported
             torch.cuda.synchronize()
             res["kernels"][name] = {"error": f"{type(exc).__name__}: {str(exc)[:300]}"}
 
     with ClockSampler(0) as clk:
         o = torch.empty_like(q)
-        record("ours_k1", lambda: ops.phase1_fwd(q, k, v, [0, m], out=o))
+        record("ours_k1", lambda: ops.phase1_fwd(q, k, v, [0, m], out=o), check=lambda out: o)
+        o32 = torch.empty(q.shape, dtype=torch.float32, device=dev)
+        record("ours_k1_f32out", lambda: ops.phase1_fwd(q, k, v, [0, m], out=o32),
+               check=lambda out: o32)
         qt, kt, vt = (x.transpose(0, 1).unsqueeze(0) for x in (q, k, v))  # [1, H, S, D] views
         from torch.nn.attention import SDPBackend, sdpa_kernel
         import torch.nn.functional as F
