@@ -49,9 +49,16 @@ struct P1Cfg {
   static constexpr int kKOff = kQOff + NQ * kTile;
   static constexpr int kVOff = kKOff + KST * kTile;
   static constexpr int kBarOff = kVOff + VST * kTile;
-  static constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 3 * NQ + 4 * NQ;
+  static constexpr int kNumBars = 1 + 2 * KST + 2 * VST + 4 * NQ + 4 * NQ;
   static constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + align slack
   static constexpr int kThreads = 64 + 128 * NQ;  // 2 control warps + softmax warpgroups
+  // 12-warp layout (NQ == 2): softmax warpgroups 0-1, then warpgroup 2 = TMA producer, MMA
+  // issuer and two idle warps; setmaxnreg moves registers from warpgroup 2 to the softmax
+  static constexpr int kThreads12 = 384;
+  static constexpr int kRegsCtl = 96, kRegsSoftmax = 200;
+  // setmaxnreg.inc draws only on what .dec released (the CTA was launched at 168 per thread):
+  // 4 warps x (168 - ctl) must cover 8 warps x (softmax - 168), or the softmax warps block
+  static_assert(4 * (168 - kRegsCtl) >= 8 * (kRegsSoftmax - 168), "register pool");
   static constexpr int kTmemCols = (NQ * (BN + D) <= 256) ? 256 : 512;
   static_assert(NQ * (BN + D) <= 512, "TMEM budget");
   static_assert(kSmem <= 232448, "shared memory budget");
@@ -69,12 +76,15 @@ struct P1Params {
   float* lse;
 };
 
+#ifndef STAR_K1_TRQ
+#define STAR_K1_TRQ 2  // TMEM lane quarter (= SM sub-partition) whose lane 0 is traced
+#endif
 #ifdef STAR_K1_TRACE
 // Timeline of CTA 0 (clock64): [head][tile][5] softmax events (S ready, max done, turn
 // granted, exps done, P handed over) and [tile][head][2] MMA events (P seen, PV+S issued).
 // Built only into the tracing library (make trace); tools/k1_trace.py reads it.
 constexpr int kTrTiles = 256;
-__device__ long long g_k1_trace[2 * kTrTiles * 5 + kTrTiles * 2 * 2];
+__device__ long long g_k1_trace[2 * kTrTiles * 5 + kTrTiles * 2 * 2 + 2 * kTrTiles * 4 * 2];
 #define K1_TR(cond, idx) \
   do {                   \
     if (cond) g_k1_trace[idx] = clock64(); \
@@ -87,8 +97,9 @@ __device__ long long g_k1_trace[2 * kTrTiles * 5 + kTrTiles * 2 * 2];
 // per-row softmax helpers (row_max, exp_pack, tmem_ld_row128, ...): softmax_tc.cuh
 
 
-template <int D, int NQ, int POLY, bool FH, int ONEP>
-__global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
+template <int D, int NQ, int POLY, int SUM, bool SPLIT, bool L12 = false, int WAIT = 0,
+          bool MW2 = false, int SWAIT = -1, bool BATCH = false>
+__global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>::kThreads, 1)
     phase1_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                      const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ P1Params prm) {
@@ -107,7 +118,8 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
   uint64_t* p_full = s_full + NQ;
   uint64_t* o_done = p_full + NQ;
   uint64_t* seq_done = o_done + NQ;  // [NQ][4]: softmax warp (i, quarter) finished its exps
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(seq_done + 4 * NQ);
+  uint64_t* p_half = seq_done + 4 * NQ;  // [NQ]: P of keys [0, BN/2) in TMEM (SPLIT)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_half + NQ);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -134,23 +146,49 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < C::KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
-    for (int i = 0; i < C::VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
+    // MW2: each q head's MMAs come from its own warp, and both release the K/V stages
+    for (int i = 0; i < C::KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], MW2 ? 2 : 1); }
+    for (int i = 0; i < C::VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], MW2 ? 2 : 1); }
     for (int i = 0; i < NQ; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
+      mbar_init(&p_half[i], 4);
       mbar_init(&o_done[i], 1);
       for (int w = 0; w < 4; ++w) mbar_init(&seq_done[i * 4 + w], 1);
     }
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<C::kTmemCols>(tmem_slot);
+  static_assert(!L12 || NQ == 2, "12-warp layout pairs two softmax warpgroups");
+  static_assert(!MW2 || L12, "two MMA warps need the 12-warp layout");
+  // TMA producer warp (also the TMEM allocator) and MMA warp(s).  MW2 spreads the MMA issue
+  // (each tcgen05.mma holds its SM sub-partition's dispatch for several cycles, which delays
+  // the softmax warps sharing it) over sub-partitions 1 and 3, the producer on 0.
+  const int ctl_warp0 = L12 ? 8 : 0;
+  const bool is_producer = warp == ctl_warp0;
+  const bool is_mma = MW2 ? (warp == 9 || warp == 11) : warp == ctl_warp0 + 1;
+  if (is_producer) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp == 0) {
+  // waits on the per-tile critical path (S ready, P handed over, MUFU turn)
+  // MMA warp waits use WAIT, softmax waits SWAIT (defaults to WAIT)
+  auto wait_mode = [](uint64_t* bar, uint32_t parity, int mode, int tag) {
+    if (mode == 3)
+      mbar_wait_dbg(bar, parity, tag);
+    else if (mode == 1)
+      mbar_wait_nohint(bar, parity);
+    else if (mode == 2)
+      mbar_wait_spin(bar, parity);
+    else
+      mbar_wait(bar, parity);
+  };
+  auto cwait = [&](uint64_t* bar, uint32_t parity, int tag = 0) { wait_mode(bar, parity, WAIT, tag); };
+  auto swait = [&](uint64_t* bar, uint32_t parity, int tag = 0) {
+    wait_mode(bar, parity, SWAIT < 0 ? WAIT : SWAIT, tag);
+  };
+  auto producer_role = [&]() {
     if (lane == 0) {
       // ================= K producer (+ Q once) =================
       tma_prefetch(&tm_q);
@@ -180,7 +218,8 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
                       kvh, k_row0 + j * C::BN);
       }
     }
-  } else if (warp == 1) {
+  };
+  auto mma_role = [&](const int i0, const int i1) {
     // ================= MMA issuer =================
     {  // the whole warp, converged: one elected lane issues each MMA / commit
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, C::BN, false, false);
@@ -189,6 +228,12 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       const uint32_t k_addr = smem_u32(smem + C::kKOff);
       const uint32_t v_addr = smem_u32(smem + C::kVOff);
       auto issue_s = [&](int i, int st) {
+        if (BATCH && D == 128) {
+          umma_ss_d128_warp(tbase + i * C::BN, umma_desc_sw128(q_addr + i * C::kTile, 16, 1024),
+                            umma_desc_sw128(k_addr + st * C::kTile, 16, 1024), idesc_s, 0u);
+          umma_commit_warp(&s_full[i]);
+          return;
+        }
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * C::kSlab + (kk & 3) * 32;
@@ -201,20 +246,46 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       mbar_wait(q_full, 0);
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
-      for (int i = 0; i < NQ; ++i) issue_s(i, 0);
+      for (int i = i0; i < i1; ++i) issue_s(i, 0);
       if (C::KST < nkv) umma_commit_warp(&k_empty[0]);
       for (int j = 0; j < nkv; ++j) {
         const int vs = j % C::VST;
-        mbar_wait(&v_full[vs], (j / C::VST) & 1);
+        cwait(&v_full[vs], (j / C::VST) & 1, 7);
         const bool next = j + 1 < nkv;
         const int ks = (j + 1) % C::KST;
-        if (next) mbar_wait(&k_full[ks], ((j + 1) / C::KST) & 1);
-        for (int i = 0; i < NQ; ++i) {
-          mbar_wait(&p_full[i], j & 1);
+        if (next) cwait(&k_full[ks], ((j + 1) / C::KST) & 1, 8);
+        for (int i = i0; i < i1; ++i) {
+          if (SPLIT) {  // P.V over keys [0, BN/2) while the softmax still exponentiates the rest
+            cwait(&p_half[i], j & 1, 2);
+            tc_fence_after();
+            if (BATCH && C::BN == 128) {
+              umma_ts_x4_warp(tbase + NQ * C::BN + i * D, tbase + i * C::BN,
+                              umma_desc_sw128(v_addr + vs * C::kTile, C::kSlab, 1024), idesc_o,
+                              j > 0 ? 1u : 0u);
+            } else
+#pragma unroll
+            for (int kk = 0; kk < C::BN / 32; ++kk) {
+              const uint64_t bd = umma_desc_sw128(v_addr + vs * C::kTile + kk * 16 * 128, C::kSlab,
+                                                  1024);
+              umma_bf16_ts_warp(tbase + NQ * C::BN + i * D, tbase + i * C::BN + kk * 8, bd,
+                                idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          cwait(&p_full[i], j & 1, 3);
           K1_TR(bx == 0 && j < 256, 2 * 256 * 5 + (j * 2 + i) * 2);
           tc_fence_after();
+          if (BATCH && C::BN == 128) {
+            if (SPLIT)
+              umma_ts_x4_warp(tbase + NQ * C::BN + i * D, tbase + i * C::BN + 32,
+                              umma_desc_sw128(v_addr + vs * C::kTile + 4 * 16 * 128, C::kSlab, 1024),
+                              idesc_o, 1u);
+            else
+              umma_ts_x8_warp(tbase + NQ * C::BN + i * D, tbase + i * C::BN,
+                              umma_desc_sw128(v_addr + vs * C::kTile, C::kSlab, 1024), idesc_o,
+                              j > 0 ? 1u : 0u);
+          } else
 #pragma unroll
-          for (int kk = 0; kk < C::BN / 16; ++kk) {
+          for (int kk = SPLIT ? C::BN / 32 : 0; kk < C::BN / 16; ++kk) {
             const uint64_t bd = umma_desc_sw128(v_addr + vs * C::kTile + kk * 16 * 128, C::kSlab,
                                                 1024);
             umma_bf16_ts_warp(tbase + NQ * C::BN + i * D, tbase + i * C::BN + kk * 8, bd, idesc_o,
@@ -230,9 +301,9 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
         if (next && j + 1 + C::KST < nkv) umma_commit_warp(&k_empty[ks]);
       }
     }
-  } else {
+  };
+  auto softmax_role = [&](const int i) {
     // ================= softmax warpgroup i =================
-    const int i = (warp - 2) >> 2;
     const int wq = warp & 3;  // TMEM lane quarter (a warp may only touch lanes 32*(warp%4)..)
     const int r = wq * 32 + lane;
     const int qrow = qt * C::BM + r;
@@ -243,36 +314,26 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
     float m_run = -INFINITY, l_run = 0.f;
 
     for (int j = 0; j < nkv; ++j) {
-      mbar_wait(&s_full[i], j & 1);
-      const bool tr = bx == 0 && threadIdx.x % 128 == 64 && j < 256;  // warp quarter 0, lane 0
+      swait(&s_full[i], j & 1, 4);
+      const bool tr = bx == 0 && wq == STAR_K1_TRQ && lane == 0 && j < 256;  // traced quarter
       K1_TR(tr, (i * 256 + j) * 5 + 0);
+      K1_TR(bx == 0 && lane == 0 && j < 256, 2 * 256 * 5 + 256 * 2 * 2 + ((i * 256 + j) * 4 + wq) * 2);
       tc_fence_after();
       const bool diag = (j == qt);
       const int lim = qrow - j * C::BN;  // columns c <= lim are visible on the diagonal tile
-      // ---- pass 1: row max (raw scores; the scale is applied once to the max) ----
-      float mx = -INFINITY;
+      // ---- row max: the whole 128-column S row in registers (four tcgen05.ld, one wait) ----
       uint32_t sv[4][32];
-      const bool spec = ONEP == 2 && j > 0;  // speculative pass against the running max
-      if (ONEP) {
-        tmem_ld_row128(s_tm, sv);
-        if (!spec) mx = (diag ? row_max_regs<true>(sv, lim) : row_max_regs<false>(sv, lim)) * sl2;
-      } else if (diag) {
-        mx = row_max<true>(s_tm, lim) * sl2;
-      } else {
-        mx = row_max<false>(s_tm, lim) * sl2;
-      }
+      tmem_ld_row128(s_tm, sv);
+      const float mx = (diag ? row_max_regs<true>(sv, lim) : row_max_regs<false>(sv, lim)) * sl2;
       K1_TR(tr, (i * 256 + j) * 5 + 1);
       float m_use = m_run, alpha = 1.f;
-      bool need = false, warp_rescale = false;
-      if (!spec) {
-        need = (j == 0) || (mx > m_run + 8.f);
-        warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
-        if (need) {
-          if (j > 0) alpha = ex2(m_run - mx);
-          m_use = mx;
-        }
+      const bool need = (j == 0) || (mx > m_run + 8.f);
+      const bool warp_rescale = (j > 0) && __any_sync(0xffffffffu, need);
+      if (need) {
+        if (j > 0) alpha = ex2(m_run - mx);
+        m_use = mx;
       }
-      // ---- pass 2: p = 2^(s*sl2 - m), row sum, bf16 P back into TMEM ----
+      // ---- p = 2^(s*sl2 - m), row sum, bf16 P back into TMEM ----
       // Ping-pong: the two warps of one SM sub-partition (head 0 and head 1, same TMEM lane
       // quarter) take turns on its MUFU pipe — head 1 exponentiates tile j after head 0 has,
       // head 0 tile j after head 1's tile j-1 — so each runs at the full exp2 rate while the
@@ -280,55 +341,41 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       const bool seq = NQ == 2 && prm.seq;
       if (seq) {
         if (i == 1)
-          mbar_wait(&seq_done[wq], j & 1);
+          swait(&seq_done[wq], j & 1, 5);
         else if (j > 0)
-          mbar_wait(&seq_done[4 + wq], (j - 1) & 1);
+          swait(&seq_done[4 + wq], (j - 1) & 1, 6);
       }
       K1_TR(tr, (i * 256 + j) * 5 + 2);
-      float rs;
-      if (spec) {
-        float mraw;
-        uint32_t pk[4][16];
-        rs = diag ? exp_pack_regs_spec<true, FH>(sv, lim, sl2, m_run, mraw, pk)
-                  : exp_pack_regs_spec<false, FH>(sv, lim, sl2, m_run, mraw, pk);
-        mx = mraw * sl2;
-        need = mx > m_run + 8.f;
-        warp_rescale = __any_sync(0xffffffffu, need);
-        if (!warp_rescale) {
+      // O is stable here: s_full(j) was committed after PV(j-1).  It is rescaled before the
+      // first P of this tile is handed over (mid-row under SPLIT, after the exps otherwise).
+      auto rescale = [&]() {
+        if (warp_rescale) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tmem_st16(s_tm + c * 16, pk[c]);
-        } else {  // rare: S is intact in TMEM; redo against the new max as the two-step form
-          if (need) {
-            alpha = ex2(m_run - mx);
-            m_use = mx;
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t orr[32];
+            tmem_ld32(o_tm + c * 32, orr);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+            tmem_st32(o_tm + c * 32, orr);
           }
-          tmem_ld_row128(s_tm, sv);
-          rs = diag ? exp_pack_regs<true, 0, FH>(sv, s_tm, lim, sl2, m_use)
-                    : exp_pack_regs<false, 0, FH>(sv, s_tm, lim, sl2, m_use);
         }
-      } else if (ONEP)
-        rs = diag ? exp_pack_regs<true, POLY, FH>(sv, s_tm, lim, sl2, m_use)
-                  : exp_pack_regs<false, POLY, FH>(sv, s_tm, lim, sl2, m_use);
-      else
-        rs = diag ? exp_pack<true, POLY, FH>(s_tm, lim, sl2, m_use)
-                  : exp_pack<false, POLY, FH>(s_tm, lim, sl2, m_use);
+      };
+      auto half = [&]() {
+        rescale();
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_half[i]);
+      };
+      const float rs = diag ? exp_pack_regs<true, POLY, SUM, SPLIT>(sv, s_tm, lim, sl2, m_use, half)
+                            : exp_pack_regs<false, POLY, SUM, SPLIT>(sv, s_tm, lim, sl2, m_use, half);
       K1_TR(tr, (i * 256 + j) * 5 + 3);
       if (seq) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&seq_done[i * 4 + wq]);
       }
-      if (warp_rescale) {
-        // O is stable: s_full(j) was committed after PV(j-1)
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t orr[32];
-          tmem_ld32(o_tm + c * 32, orr);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
-          tmem_st32(o_tm + c * 32, orr);
-        }
-      }
+      if (!SPLIT) rescale();
       tmem_wait_st();
       l_run = l_run * alpha + rs;
       m_run = m_use;
@@ -336,6 +383,8 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[i]);
       K1_TR(tr, (i * 256 + j) * 5 + 4);
+      // every warp quarter: S seen and P handed over (skew across SM sub-partitions)
+      K1_TR(bx == 0 && lane == 0 && j < 256, 2 * 256 * 5 + 256 * 2 * 2 + ((i * 256 + j) * 4 + wq) * 2 + 1);
     }
     // ---- epilogue: O / l -> rows; lse = ln(sum) + max ----
     mbar_wait(&o_done[i], 0);  // one phase: the commit after the last P.V
@@ -380,21 +429,39 @@ __global__ void __launch_bounds__(P1Cfg<D, NQ>::kThreads, 1)
       for (int t = 0; t < n_dst; ++t)
         prm.lse[(int64_t)(h0 + i) * prm.lse_stride + prm.segs.q_row0[t == 0 ? s : t] + qrow] = lv;
     }
+  };
+  if (L12) {
+    // setmaxnreg inside warpgroup-uniform branches (the warpgroup index is made provably
+    // uniform by a shuffle), so ptxas allocates each role's code with its own budget
+    const int wg = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 7), 0);
+    if (wg == 2) {
+      regs_dealloc<C::kRegsCtl>();
+      if (is_producer)
+        producer_role();
+      else if (is_mma)
+        MW2 ? mma_role(warp == 9 ? 0 : 1, warp == 9 ? 1 : 2) : mma_role(0, NQ);
+    } else {
+      regs_alloc<C::kRegsSoftmax>();
+      softmax_role(wg);
+    }
+  } else {
+    if (is_producer)
+      producer_role();
+    else if (is_mma)
+      mma_role(0, NQ);
+    else
+      softmax_role((warp - 2) >> 2);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (is_producer) {
     __syncwarp();
     tmem_free<C::kTmemCols>(tbase);
   }
 }
 
 // ------------------------------------------------------------------ host
-constexpr int kDefaultPoly = 0;
 constexpr int kDefaultSeq = 1;
-constexpr int kDefaultFH = 1;
-constexpr int kDefaultOnePass = 1;
-constexpr int kDefaultSpec = 0;  // speculative one-pass softmax (STAR_K1_SPEC)
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -456,14 +523,36 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
                                  std::max(segs.tile_lo[i], i > 0 ? segs.dedup_tiles : 0);
   const int tiles = prm.segs.tile_start[segs.n];
   if (tiles == 0) return STAR_OK;
-  // the product build instantiates only the measured-best softmax (one-pass row,
-  // f32 += bf16 row sums, MUFU ping-pong of the two heads, no FMA exp2 share)
+  // the product build instantiates the measured-best form: one-pass row in
+  // registers, split P hand-off, fp32 FADD2 row sums, every 4th exponential pair on the FMA
+  // pipe, MUFU ping-pong of the two heads; NQ == 2 runs the 12-warp layout (setmaxnreg gives
+  // the softmax warpgroups 200 registers) with the MMA warp waiting without a suspend hint
   prm.seq = kDefaultSeq;
-  const auto kern = phase1_tc_kernel<D, NQ, kDefaultPoly, kDefaultFH != 0, kDefaultOnePass>;
+  using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const P1Params);
+  KernT kern;
+  int threads;
+  if constexpr (NQ == 2) {
+    kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0>;
+    threads = C::kThreads12;
+  } else {
+    kern = phase1_tc_kernel<D, NQ, 4, 2, true, false, 1, false, 0>;
+    threads = C::kThreads;
+  }
+  if (const char* sv = getenv("STAR_K1_SM")) {  // measurement knob (tools/phase1_bench.py)
+    const int vv = atoi(sv);
+    if (vv == 1) {  // round-1 form: 10 warps, f32 += bf16 row sums, whole-P hand-off
+      kern = phase1_tc_kernel<D, NQ, 0, 1, false>;
+      threads = C::kThreads;
+    }
+    if constexpr (NQ == 2) {
+      if (vv == 2) kern = phase1_tc_kernel<D, NQ, 0, 2, true, true, 1, false, 0>;
+      if (vv == 3) kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0, true>;
+    }
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
   dim3 grid(tiles * hkv * (hq / hkv / NQ));
-  kern<<<grid, C::kThreads, C::kSmem, stream>>>(tq, tk, tv, prm);
+  kern<<<grid, threads, C::kSmem, stream>>>(tq, tk, tv, prm);
   STAR_LAUNCH_CHECK("phase1_tc");
   return STAR_OK;
 }

@@ -11,32 +11,6 @@ namespace star {
 using namespace sm100;
 
 
-// Softmax pass 1 over one 128-column S row in TMEM: max of the (masked) raw scores.
-// Loads are software-pipelined: chunk c+1 is in flight while chunk c is reduced.
-template <bool DIAG>
-__device__ __forceinline__ float row_max(uint32_t s_tm, int lim) {
-  uint32_t buf[2][32];
-  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-  tmem_ld32(s_tm, buf[0]);
-  tmem_wait_ld_tied(buf[0]);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    if (c < 3) tmem_ld32(s_tm + (c + 1) * 32, buf[(c + 1) & 1]);
-    uint32_t* a = buf[c & 1];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      float v0 = __uint_as_float(a[e]), v1 = __uint_as_float(a[e + 1]);
-      if (DIAG) {
-        if (c * 32 + e > lim) v0 = -INFINITY;
-        if (c * 32 + e + 1 > lim) v1 = -INFINITY;
-      }
-      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(v0, v1));
-    }
-    if (c < 3) tmem_wait_ld_tied(buf[(c + 1) & 1]);
-  }
-  return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-}
-
 // 2^x for a pair on the FMA pipe (offloads the MUFU/XU pipe): x clamped to >= -125,
 // x = n + f with n = round(x) (magic-number rounding), 2^f by a degree-3 minimax
 // polynomial on [-1/2, 1/2] (max rel. error 2.1e-4, below bf16's 2^-9 rounding of P),
@@ -78,53 +52,6 @@ __device__ __forceinline__ void acc_bf16x2(float& lo_acc, float& hi_acc, uint32_
       : "r"(w));
 }
 
-template <bool DIAG, int POLY, bool FH>
-__device__ __forceinline__ float exp_pack(uint32_t s_tm, int lim, float sl2, float m) {
-  float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
-  uint32_t buf[2][32];
-  tmem_ld32(s_tm, buf[0]);
-  tmem_wait_ld_tied(buf[0]);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    // chunk c+1 loads while chunk c is exponentiated; P of chunk c goes to columns
-    // [16c, 16c+16), all below the columns still being read
-    if (c < 3) tmem_ld32(s_tm + (c + 1) * 32, buf[(c + 1) & 1]);
-    const uint32_t* sv = buf[c & 1];
-    uint32_t pk[16];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      const float2 x = ffma2(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), sc2, nm2);
-      float p0, p1;
-      if (c >= 4 - POLY) {
-        const float2 p = poly_ex2x2(x);
-        p0 = p.x;
-        p1 = p.y;
-      } else {
-        p0 = ex2(x.x);
-        p1 = ex2(x.y);
-      }
-      if (DIAG) {
-        const int col = c * 32 + e;
-        if (col > lim) p0 = 0.f;
-        if (col + 1 > lim) p1 = 0.f;
-      }
-      // the row sum uses the bf16-rounded p that the P.V MMA will see, so numerator and
-      // denominator weight each key identically (a dominant key then carries no error)
-      const uint32_t w = pack_bf16x2(p0, p1);
-      pk[e >> 1] = w;
-      float2& acc = rsum[(e >> 1) & 1];
-      if (FH)
-        acc_bf16x2(acc.x, acc.y, w);
-      else
-        acc = fadd2(acc, make_float2(bf16lo(w), bf16hi(w)));
-    }
-    tmem_st16(s_tm + c * 16, pk);
-    if (c < 3) tmem_wait_ld_tied(buf[(c + 1) & 1]);
-  }
-  return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
-}
-
 // One-pass softmax: the whole 128-column S row is loaded into registers once (four
 // tcgen05.ld in flight together, one wait), reduced to its max, then exponentiated in
 // place — no second TMEM read and a single exposed load latency per tile.
@@ -156,9 +83,21 @@ __device__ __forceinline__ float row_max_regs(const uint32_t (&sv)[4][32], int l
   return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
 }
 
-template <bool DIAG, int POLY, bool FH>
+// Row-sum forms (SUM): 0 = fp32 FADD2 over the unpacked bf16-rounded p, 1 = f32 += bf16
+// (FHADD.BF16, one per element), 2 = fp32 FADD2 over the unrounded p (half the instructions
+// of 1; the bf16 quantisation of P then only enters the numerator, which measured the same
+// error against the fp64 oracle, tests/test_tolerance.py).
+// POLY (> 0): every POLY-th exponential pair runs on the FMA pipe (poly_ex2x2), spread
+// evenly through the row so the FMA work fills the single warp's MUFU issue gaps.
+// SPLIT: once the P of keys [0, 64) is stored, mid() runs (the caller hands that half over,
+// so the P.V of those keys overlaps the exponentials of the rest); chunks 0-1 of S are dead
+// by then, which leaves registers for whatever mid() needs.
+struct NoMid {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <bool DIAG, int POLY, int SUM, bool SPLIT = false, class Mid = NoMid>
 __device__ __forceinline__ float exp_pack_regs(const uint32_t (&sv)[4][32], uint32_t s_tm, int lim,
-                                               float sl2, float m) {
+                                               float sl2, float m, const Mid& mid = Mid()) {
   float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
 #pragma unroll
@@ -170,7 +109,7 @@ __device__ __forceinline__ float exp_pack_regs(const uint32_t (&sv)[4][32], uint
     for (int e = 0; e < 32; e += 2) {
       const float2 x = ffma2(make_float2(__uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1])),
                              sc2, nm2);
-      if (c >= 4 - POLY) {
+      if (POLY > 0 && ((c * 16 + (e >> 1)) % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY - 1 : 0)) {
         const float2 q = poly_ex2x2(x);
         p[e] = q.x;
         p[e + 1] = q.y;
@@ -191,64 +130,16 @@ __device__ __forceinline__ float exp_pack_regs(const uint32_t (&sv)[4][32], uint
       const uint32_t w = pack_bf16x2v(p0, p1);
       pk[e >> 1] = w;
       float2& acc = rsum[(e >> 1) & 1];
-      if (FH)
+      if (SUM == 1)
         acc_bf16x2(acc.x, acc.y, w);
+      else if (SUM == 2)
+        acc = fadd2(acc, make_float2(p0, p1));
       else
         acc = fadd2(acc, make_float2(bf16lo(w), bf16hi(w)));
     }
     tmem_st16(s_tm + c * 16, pk);
+    if (SPLIT && c == 1) mid();
   }
-  return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
-}
-
-// Speculative one-pass softmax (ONEP == 2, tiles after the first): exponentiate against the
-// running max m straight away and take the row max of the raw scores in the same pass (the
-// FMNMX3 work fills issue slots of the MUFU-bound loop instead of a pass before it).  P is
-// packed into registers but NOT stored: the caller stores it unless the new max exceeds m by
-// more than the lazy-rescale threshold — the case in which the two-step kernel uses the new
-// max — and then reloads S (still intact in TMEM) and redoes the exps, so P and the row
-// sums are bit-identical to the two-step form.  Register peak as the one-pass form: each
-// chunk's S registers die as its packed P is born.
-template <bool DIAG, bool FH>
-__device__ __forceinline__ float exp_pack_regs_spec(const uint32_t (&sv)[4][32], int lim,
-                                                    float sl2, float m, float& mraw,
-                                                    uint32_t (&pk)[4][16]) {
-  float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
-  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float p[32];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      float v0 = __uint_as_float(sv[c][e]), v1 = __uint_as_float(sv[c][e + 1]);
-      const float2 x = ffma2(make_float2(v0, v1), sc2, nm2);
-      p[e] = ex2v(x.x);
-      p[e + 1] = ex2v(x.y);
-      if (DIAG) {
-        if (c * 32 + e > lim) v0 = -INFINITY;
-        if (c * 32 + e + 1 > lim) v1 = -INFINITY;
-      }
-      m4[(e >> 1) & 3] = fmaxf(m4[(e >> 1) & 3], fmaxf(v0, v1));
-    }
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      float p0 = p[e], p1 = p[e + 1];
-      if (DIAG) {
-        const int col = c * 32 + e;
-        if (col > lim) p0 = 0.f;
-        if (col + 1 > lim) p1 = 0.f;
-      }
-      const uint32_t w = pack_bf16x2v(p0, p1);
-      pk[c][e >> 1] = w;
-      float2& acc = rsum[(e >> 1) & 1];
-      if (FH)
-        acc_bf16x2(acc.x, acc.y, w);
-      else
-        acc = fadd2(acc, make_float2(bf16lo(w), bf16hi(w)));
-    }
-  }
-  mraw = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
   return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
 }
 

@@ -35,13 +35,14 @@ out = torch.empty_like(q)
 for _ in range(3):
     ops.phase1_fwd(q, k, v, seg, out=out)
 torch.cuda.synchronize()
-N = 2 * 256 * 5 + 256 * 2 * 2
+N = 2 * 256 * 5 + 256 * 2 * 2 + 2 * 256 * 4 * 2
 buf = (ctypes.c_longlong * N)()
 lib.star_debug_k1_trace.restype = ctypes.c_int
 assert lib.star_debug_k1_trace(buf, N) == N
 a = np.frombuffer(buf, dtype=np.int64).copy()
 sm = a[:2 * 256 * 5].reshape(2, 256, 5)
-mm = a[2 * 256 * 5:].reshape(256, 2, 2)
+mm = a[2 * 256 * 5:2 * 256 * 5 + 256 * 4].reshape(256, 2, 2)
+wq = a[2 * 256 * 5 + 256 * 4:].reshape(2, 256, 4, 2)  # [head][tile][quarter][S seen, P out]
 ntiles = b // 128
 t0 = min(sm[0, 0, 0], sm[1, 0, 0])
 print("tile  head: S_ready max_done turn exps_done P_out | mma: P_seen issued   (clk from t0)")
@@ -60,6 +61,11 @@ stat = {
     "handoff": float((sm[:, rng, 4] - sm[:, rng, 3]).mean()),
     "p_to_next_s": float((sm[:, 9:ntiles - 3, 0] - sm[:, 8:ntiles - 4, 4]).mean()),
     "mma_issue": float((mm[rng, :, 1] - mm[rng, :, 0]).mean()),
+    "p_out_to_mma_seen": float((mm[rng, :, 0] - sm[:, rng, 4].T).mean()),
+    "quarter_s_seen_minus_min": [float(x) for x in (wq[:, rng, :, 0] - wq[:, rng, :, 0].min(axis=2, keepdims=True)).mean(axis=(0, 1))],
+    "quarter_p_out_minus_min": [float(x) for x in (wq[:, rng, :, 1] - wq[:, rng, :, 1].min(axis=2, keepdims=True)).mean(axis=(0, 1))],
+    "mma_seen_minus_last_quarter_p": float((mm[rng, :, 0] - wq[:, rng, :, 1].max(axis=2).T).mean()),
+    "issued_to_next_s": float((sm[:, 9:ntiles - 3, 0].T - mm[8:ntiles - 4, :, 1]).mean()),
     "knobs": {k_: v_ for k_, v_ in os.environ.items() if k_.startswith("STAR_K1_")},
 }
 print(json.dumps(stat))

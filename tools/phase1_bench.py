@@ -33,13 +33,19 @@ for _ in range(2):
     ops.phase1_fwd(q, k, v, seg, out=out)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-for _ in range(a.iters):
-    ops.phase1_fwd(q, k, v, seg, out=out)
-e1.record()
-torch.cuda.synchronize()
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import ClockSampler  # noqa: E402
+
+with ClockSampler(0) as clk:
+    e0.record()
+    for _ in range(a.iters):
+        ops.phase1_fwd(q, k, v, seg, out=out)
+    e1.record()
+    torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.iters
+mhz = clk.summary()["sm_mhz"] or float("nan")
 knobs = " ".join(f"{k}={os.environ[k]}" for k in sorted(os.environ) if k.startswith("STAR_K1_"))
-print(f"{knobs or 'defaults'} ms={ms:.2f} TFLOP/s={flops / ms / 1e9:.1f}")
+print(f"{knobs or 'defaults'} ms={ms:.2f} TFLOP/s={flops / ms / 1e9:.1f} sm_mhz={mhz:.0f} "
+      f"Mclk={ms * mhz / 1e3:.2f} flop/clk/SM={flops / (ms * 1e-3 * mhz * 1e6) / 148:.0f}")
 if a.save:
     torch.save(out.cpu(), a.save)

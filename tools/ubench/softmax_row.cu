@@ -58,7 +58,8 @@ __global__ void kern(float* out, int iters, long long* cyc) {
       for (int e = 0; e < 32; e += 2) {
         float2 x = ffma2(make_float2(sv[c * 32 + e], sv[c * 32 + e + 1]), sc2, nm2);
         const bool poly = MODE == 2 || MODE == 3 ? c >= 6 - MODE
-                        : MODE == 4 ? ((e >> 1) & 3) == 3 : MODE == 5 ? ((e >> 1) & 7) == 7 : false;
+                        : (MODE == 4 || MODE == 7) ? ((e >> 1) & 3) == 3
+                        : MODE == 5 ? ((e >> 1) & 7) == 7 : false;
         if (poly) {  // MODE 2: chunk 3 on FMA; 3: chunks 2-3; 4: every 4th pair; 5: every 8th
           float2 q = poly_ex2x2(x);
           p[e] = q.x;
@@ -72,7 +73,10 @@ __global__ void kern(float* out, int iters, long long* cyc) {
       for (int e = 0; e < 32; e += 2) {
         uint32_t w = pack(p[e], p[e + 1]);
         chk ^= w;
-        if (MODE >= 1) acc2(rs[(e >> 1) & 1].x, rs[(e >> 1) & 1].y, w);
+        if (MODE >= 6)
+          rs[(e >> 1) & 1] = fadd2(rs[(e >> 1) & 1], make_float2(p[e], p[e + 1]));
+        else if (MODE >= 1)
+          acc2(rs[(e >> 1) & 1].x, rs[(e >> 1) & 1].y, w);
       }
     }
     tot += rs[0].x + rs[0].y + rs[1].x + rs[1].y;
@@ -85,15 +89,15 @@ __global__ void kern(float* out, int iters, long long* cyc) {
 int main() {
   float* out; long long* cyc; cudaMalloc(&out, 148 * 1024 * 4); cudaMalloc(&cyc, 8);
   const int iters = 2048;
-  for (int mode = 0; mode < 6; ++mode)
+  for (int mode = 0; mode < 8; ++mode)
     for (int wps = 1; wps <= 3; ++wps) {
       auto k = mode == 0 ? kern<0> : mode == 1 ? kern<1> : mode == 2 ? kern<2> : mode == 3 ? kern<3>
-             : mode == 4 ? kern<4> : kern<5>;
+             : mode == 4 ? kern<4> : mode == 5 ? kern<5> : mode == 6 ? kern<6> : kern<7>;
       k<<<148, 128 * wps>>>(out, 8, cyc);
       k<<<148, 128 * wps>>>(out, iters, cyc);
       long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
       printf("mode=%s warps/SMSP=%d: %.1f clk per 128-score row per warp (MUFU floor 1024 x warps)\n",
-             mode == 0 ? "exp+pack" : mode == 1 ? "exp+pack+sum" : mode == 2 ? "+sum, 1/4 poly" : mode == 3 ? "+sum, 1/2 poly" : mode == 4 ? "+sum, 1/4 poly spread" : "+sum, 1/8 poly spread", wps, (double)c / iters);
+             mode == 0 ? "exp+pack" : mode == 1 ? "exp+pack+sum" : mode == 2 ? "+sum, 1/4 poly" : mode == 3 ? "+sum, 1/2 poly" : mode == 4 ? "+sum, 1/4 poly spread" : mode == 5 ? "+sum, 1/8 poly spread" : mode == 6 ? "fadd2 sum" : "fadd2 sum, 1/4 poly spread", wps, (double)c / iters);
     }
   return 0;
 }
