@@ -703,15 +703,22 @@ def decode_layers_step(dev, world, rank, own_rows, ex, k2_us, barrier, max_over_
     import torch.distributed as tdist
 
     group = tdist.group.WORLD if (world > 1 and ex is None) else None
-    table = ops.RopeTable(L, room, d, 10000.0, dev)  # cos/sin of the decode positions
+    table = ops.DecodeRope(L, room, d, 10000.0, 1, dev)  # cos/sin of the decode positions
     attend = paged_attend(pool, appends=rank == q_rank, max_rows=own_rows + room, theta=10000.0,
                           heads=hq, exchange=ex, group=group, rope_table=table)
     launches = [0]
 
+    finish = getattr(attend, "finish", None)  # fused decode: counters + position, one launch
+    if getattr(attend, "prime", None) is not None:
+        attend.prime(pos)
+
     def step():
         for li in range(n_layers):
             attend(li, qn[li], kn[li], vn[li], pos)
-        pos.add_(1)
+        if finish is not None:
+            finish(pos)
+        else:
+            pos.add_(1)
 
     step()  # eager: workspaces sized before capture
     torch.cuda.synchronize(dev)
@@ -738,9 +745,13 @@ def decode_layers_step(dev, world, rank, own_rows, ex, k2_us, barrier, max_over_
            "k2_kernel_us_per_layer": k2_us, "overhead_over_k2": us / n_layers / k2_us - 1.0,
            "hbm_frac_per_layer": kv_bytes / (us / n_layers * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6532.9),
            "tokens_timed": tokens, "cached_rows_per_rank": own_rows,
-           "path": "decoding.paged_attend per layer (query rank: star_kv_append at the "
-                   "device row counter, RoPE from the decode-position table; K2" + (" with the fused peer exchange" if ex is not None
-                                                 else "") + "), 32 layers in one CUDA graph per token"}
+           "path": ("decoding.paged_attend per layer: " +
+                    ("ONE star_phase2_decode launch (RoPE of q in every K2 CTA, the query rank's "
+                     "new k/v row written by the K2 CTA that streams it" if finish is not None
+                     else "star_kv_append + K2") +
+                    (", fused peer exchange" if ex is not None else "") +
+                    "), star_decode_advance once per token, 32 layers in one CUDA graph per token"),
+           "launches_per_token": n_layers + 1 if finish is not None else 2 * n_layers + 1}
     del pool, g
     torch.cuda.empty_cache()
     return res
@@ -762,6 +773,7 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
     from paper_2411_17116_b200 import ops
 
     page = 128
+    LPT = 8  # fused decode launches per graph step (layers sharing one star_decode_advance)
     Bs, Ss, Gs = (1, 2, 4, 8, 16, 32), (32768, 131072, 262144, 1048576), (1, 2, 4, 8)
     kern = {}
     for B in Bs:
@@ -782,13 +794,17 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
             kv_len = torch.full((B,), rows, dtype=torch.int32, device=dev)
             ws = ops.Phase2Workspace()
             maxk = rows + n_tokens
-            rtab = ops.RopeTable(rows, n_tokens + 8, d, 10000.0, dev)
+            rtab = ops.DecodeRope(rows, n_tokens + 8, d, 10000.0, B, dev)
+            rtab.prime(pos)
 
             def step():
-                qr = ops.kv_append(q.view(B, hq, d), kn, vn, pos, kv_len, kp, vp, table,
-                                   table=rtab)
-                ops.phase2_partial(qr.view(B, 1, hq, d), kp, vp, table, kv_len, maxk, workspace=ws)
-                pos.add_(1)
+                # LPT layers' worth of fused decode launches over this cache (each attends
+                # over kv_len + 1 rows and writes the token's row), then the once-per-token
+                # counter / position advance — per layer = step / LPT, as in a model step
+                for _ in range(LPT):
+                    ops.phase2_decode(q.view(B, hq, d), kn, vn, pos, kp, vp, table, kv_len, maxk,
+                                      table=rtab, workspace=ws)
+                ops.decode_advance(kv_len, pos, rope=rtab)
 
             step()
             side = torch.cuda.Stream(dev)
@@ -799,6 +815,7 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
             torch.cuda.current_stream(dev).wait_stream(side)
             kv_len.fill_(rows)
             pos.fill_(rows)
+            rtab.prime(pos)
             torch.cuda.synchronize(dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -806,7 +823,7 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
                 g.replay()
             e1.record()
             torch.cuda.synchronize(dev)
-            us = e0.elapsed_time(e1) / n_tokens * 1e3
+            us = e0.elapsed_time(e1) / n_tokens / LPT * 1e3
             nbytes = B * (rows + n_tokens / 2) * hkv * d * 2 * 2  # mean cache over the 64 tokens
             kern[(B, rows)] = (us, nbytes / us / 1e3)
             del kp, vp, g
@@ -818,13 +835,23 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
             lses = ops.prng_fill((G, B * hq), 27, 1, 1.0, torch.float32, dev)
             ops.merge(outs, lses)
             torch.cuda.synchronize(dev)
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            gm = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side), torch.cuda.graph(gm, stream=side):
+                for _ in range(20):
+                    ops.merge(outs, lses)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            gm.replay()
+            torch.cuda.synchronize(dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for _ in range(50):
-                ops.merge(outs, lses)
+            for _ in range(5):
+                gm.replay()
             e1.record()
             torch.cuda.synchronize(dev)
-            merge_us[(B, G)] = e0.elapsed_time(e1) / 50 * 1e3
+            merge_us[(B, G)] = e0.elapsed_time(e1) / 100 * 1e3
+            del gm
     out = []
     for B in Bs:
         for S in Ss:
@@ -839,8 +866,10 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
                             "frac_of_measured_hbm": k[1] / hbm_peak,
                             "merge_us": merge_us.get((B, G))})
     return {"points": out, "tokens": n_tokens,
-            "timing": "per (B, S/G): CUDA graph of star_kv_append (B rows) + K2 over B paged "
-                      "caches, replayed for 64 generated tokens; merge_us = K3 over G partials"}
+            "timing": "per (B, S/G): CUDA graph of 8 star_phase2_decode launches (RoPE + append "
+                      "of the B new rows inside K2 over the B paged caches, one per layer) + one "
+                      "star_decode_advance, replayed for 64 generated tokens; value per layer = "
+                      "graph / 8; merge_us = K3 over G partials (graph-replayed launches)"}
 
 
 def cfg1_session(dev):

@@ -101,6 +101,52 @@ int star_kv_append(const void* q_in, const void* k_in, const void* v_in, int dty
                    int64_t table_pos0, int64_t table_positions, void* stream);
 
 /*
+ * Fused decode step of one layer (BF16, one new token per sequence, paged cache as
+ * star_phase2_partial): q_raw [batch][hq][d] / k_new, v_new [batch][hkv][d] are the token's
+ * PRE-RoPE projections (row strides q_stride / kv_stride elements), positions[batch] its
+ * device positions.  Every K2 CTA rotates its q heads itself (RoPE through rope_table_cs when
+ * the position is inside it, else the fp64 angle, as star_rope); with append != 0 the CTA
+ * whose key range holds row kv_len[b] writes the rotated k and raw v there and K2 attends over
+ * kv_len[b] + 1 rows — the append-then-attend of ss/sim.py:275-277 in ONE launch instead of
+ * star_kv_append + star_phase2_partial.  kv_len is NOT advanced (call star_decode_advance
+ * once per token); append == 0 rotates q only (a rank that is not the query host).
+ * rope_cur_cs (nullable): double [batch][d/2][2] cos/sin at positions[b], as
+ * star_decode_advance maintains it — read directly, so no load waits on the position.
+ * Results are bit-identical to star_kv_append followed by star_phase2_partial.
+ */
+int star_phase2_decode(const void* q_raw, const void* k_new, const void* v_new, int append,
+                       int64_t q_stride, int64_t kv_stride, const int64_t* positions, double theta,
+                       const double* rope_table_cs, int64_t table_pos0, int64_t table_positions,
+                       const double* rope_cur_cs, int batch, int hq, int hkv, int d, const void* k_pages, const void* v_pages,
+                       int64_t num_pages, const int32_t* page_table, int pages_per_seq,
+                       int page_size, const int32_t* kv_len, int64_t max_kv_len, float* out,
+                       float* lse, int n_splits, void* workspace, void* stream);
+
+/* star_phase2_decode with the fused peer exchange of star_phase2_exchange (C1 fused). */
+int star_phase2_decode_exchange(const void* q_raw, const void* k_new, const void* v_new,
+                                int append, int64_t q_stride, int64_t kv_stride,
+                                const int64_t* positions, double theta,
+                                const double* rope_table_cs, int64_t table_pos0,
+                                int64_t table_positions, const double* rope_cur_cs, int batch,
+                                int hq, int hkv, int d,
+                                const void* k_pages, const void* v_pages, int64_t num_pages,
+                                const int32_t* page_table, int pages_per_seq, int page_size,
+                                const int32_t* kv_len, int64_t max_kv_len, float* out, float* lse,
+                                int n_splits, void* workspace, void* const* boxes, int world,
+                                int64_t cap_rows, int cap_groups, int rank, void* stream);
+
+/*
+ * End of a fused decode token: kv_len[0..n_counters) += add, positions[0..n_positions) += inc,
+ * then (cur_cs != NULL) cur_cs[b] = cos/sin of the new positions[b] (d/2 pairs; from the
+ * table when inside it, else the fp64 angle) for the next token's star_phase2_decode.
+ * inc = add = 0 only fills cur_cs (before the first token).
+ */
+int star_decode_advance(int32_t* kv_len, int n_counters, int add, int64_t* positions,
+                        int n_positions, int inc, double* cur_cs, const double* rope_table_cs,
+                        int64_t table_pos0, int64_t table_positions, int d, double theta,
+                        void* stream);
+
+/*
  * RoPE cos/sin table for positions [pos0, pos0 + n_positions): cs[(p*d/2 + i)*2 + {0,1}] =
  * {cos, sin} of (pos0 + p) * theta^(-2i/d), fp64, the same expression star_rope evaluates
  * (ss/numerics.py:173-176), so star_kv_append through the table (rope_table_cs != NULL and

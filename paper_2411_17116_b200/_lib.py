@@ -33,6 +33,20 @@ SIGNATURES = {
                                c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p,
                                c_int64, c_int64, c_void_p]),
     "star_rope_table": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_void_p]),
+    "star_phase2_decode": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p,
+                                   c_double, c_void_p, c_int64, c_int64, c_void_p, c_int, c_int,
+                                   c_int, c_int,
+                                   c_void_p, c_void_p, c_int64, c_void_p, c_int, c_int, c_void_p,
+                                   c_int64, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
+    "star_phase2_decode_exchange": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int64,
+                                            c_void_p, c_double, c_void_p, c_int64, c_int64,
+                                            c_void_p, c_int,
+                                            c_int, c_int, c_int, c_void_p, c_void_p, c_int64,
+                                            c_void_p, c_int, c_int, c_void_p, c_int64, c_void_p,
+                                            c_void_p, c_int, c_void_p, c_void_p, c_int, c_int64,
+                                            c_int, c_int, c_void_p]),
+    "star_decode_advance": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p,
+                                    c_void_p, c_int64, c_int64, c_int, c_double, c_void_p]),
     "star_phase1_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, POINTER(c_int64),
                                 c_int, c_int, c_int, c_int64, c_int64, c_void_p, c_int, c_int64,
                                 c_void_p, c_int64, c_void_p]),

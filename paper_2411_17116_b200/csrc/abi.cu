@@ -62,7 +62,10 @@ int64_t phase2_workspace_bytes(int, int, int, int, int);
 int phase2_auto_splits(int, int, int64_t, int);
 int phase2_partial(const void*, int, int, int, int, int, int, const void*, const void*, int,
                    int64_t, const int32_t*, int, int, const int32_t*, int64_t, int, float*, float*,
-                   int, void*, const PeerPush*, int*, cudaStream_t);
+                   int, void*, const PeerPush*, int*, cudaStream_t,
+                   const DecodeAppend* dap = nullptr);
+int decode_advance(int32_t*, int, int, int64_t*, int, int, void*, const void*, int64_t, int64_t,
+                   int, double, cudaStream_t);
 int check_exchange(const ExchangeLayout&, void* const*, int, int64_t, int);
 PeerPush make_push(const ExchangeLayout&, void* const*, int);
 int exchange_push(const float*, const float*, int, int, int, int, int, void* const*,
@@ -320,6 +323,108 @@ int star_phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, i
                         page_table,
                         pages_per_seq, page_size, kv_len, max_kv_len, own_tail, out, lse, n_splits,
                         workspace, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+static DecodeAppend make_decode_append(const void* q_raw, const void* k_new, const void* v_new,
+                                       int64_t q_stride, int64_t kv_stride, const int64_t* positions,
+                                       const double* rope_table_cs, int64_t table_pos0,
+                                       int64_t table_positions, double theta, int append,
+                                       const double* cur_cs) {
+  DecodeAppend ap{};
+  ap.cur_cs = cur_cs;
+  ap.q_raw = q_raw;
+  ap.k_new = k_new;
+  ap.v_new = v_new;
+  ap.q_rs = q_stride;
+  ap.kv_rs = kv_stride;
+  ap.pos = positions;
+  ap.rtab = rope_table_cs;
+  ap.rtab_pos0 = table_pos0;
+  ap.rtab_n = rope_table_cs != nullptr ? table_positions : 0;
+  ap.theta = theta;
+  ap.on = 1;
+  ap.add = append ? 1 : 0;
+  return ap;
+}
+
+static int check_decode_args(const void* q_raw, const void* k_new, const void* v_new, int append,
+                             const int64_t* positions, int hq, int hkv, int d, int64_t q_stride,
+                             int64_t kv_stride, double theta) {
+  if (q_raw == nullptr || positions == nullptr) return fail(STAR_ESHAPE, "phase2 decode: NULL q / positions");
+  if (append && (k_new == nullptr || v_new == nullptr))
+    return fail(STAR_ESHAPE, "phase2 decode: append needs the new k / v rows");
+  if (q_stride < (int64_t)hq * d || (append && kv_stride < (int64_t)hkv * d))
+    return fail(STAR_ESHAPE, "phase2 decode: row stride smaller than heads*d");
+  if ((q_stride | kv_stride) & 1) return fail(STAR_ECONFIG, "phase2 decode: odd row strides");
+  if (!(theta > 0)) return fail(STAR_ECONFIG, "rope theta must be positive, got %g", theta);
+  return STAR_OK;
+}
+
+int star_phase2_decode(const void* q_raw, const void* k_new, const void* v_new, int append,
+                       int64_t q_stride, int64_t kv_stride, const int64_t* positions, double theta,
+                       const double* rope_table_cs, int64_t table_pos0, int64_t table_positions,
+                       const double* rope_cur_cs, int batch, int hq, int hkv, int d, const void* k_pages, const void* v_pages,
+                       int64_t num_pages, const int32_t* page_table, int pages_per_seq,
+                       int page_size, const int32_t* kv_len, int64_t max_kv_len, float* out,
+                       float* lse, int n_splits, void* workspace, void* stream) {
+  int rc = check_heads(hq, hkv, d);
+  if (rc) return rc;
+  if ((rc = check_decode_args(q_raw, k_new, v_new, append, positions, hq, hkv, d, q_stride,
+                              kv_stride, theta)))
+    return rc;
+  const DecodeAppend ap = make_decode_append(q_raw, k_new, v_new, q_stride, kv_stride, positions,
+                                             rope_table_cs, table_pos0, table_positions, theta,
+                                             append, rope_cur_cs);
+  return phase2_partial(q_raw, STAR_BF16, batch, 1, hq, hkv, d, k_pages, v_pages, STAR_BF16,
+                        num_pages, page_table, pages_per_seq, page_size, kv_len, max_kv_len, 0, out,
+                        lse, n_splits, workspace, nullptr, nullptr, (cudaStream_t)stream, &ap);
+}
+
+int star_phase2_decode_exchange(const void* q_raw, const void* k_new, const void* v_new,
+                                int append, int64_t q_stride, int64_t kv_stride,
+                                const int64_t* positions, double theta,
+                                const double* rope_table_cs, int64_t table_pos0,
+                                int64_t table_positions, const double* rope_cur_cs, int batch,
+                                int hq, int hkv, int d,
+                                const void* k_pages, const void* v_pages, int64_t num_pages,
+                                const int32_t* page_table, int pages_per_seq, int page_size,
+                                const int32_t* kv_len, int64_t max_kv_len, float* out, float* lse,
+                                int n_splits, void* workspace, void* const* boxes, int world,
+                                int64_t cap_rows, int cap_groups, int rank, void* stream) {
+  int rc = check_heads(hq, hkv, d);
+  if (rc) return rc;
+  if (batch < 1) return fail(STAR_ESHAPE, "phase2: bad batch");
+  if (out == nullptr || lse == nullptr) return fail(STAR_ESHAPE, "phase2 exchange: NULL out/lse");
+  if ((rc = check_decode_args(q_raw, k_new, v_new, append, positions, hq, hkv, d, q_stride,
+                              kv_stride, theta)))
+    return rc;
+  const ExchangeLayout L{world, cap_rows, d, cap_groups};
+  rc = check_exchange(L, boxes, rank, (int64_t)batch * hq, batch * hkv);
+  if (rc) return rc;
+  PeerPush pp = make_push(L, boxes, rank);
+  pp.merge = 1;
+  int merged = 0;
+  const DecodeAppend ap = make_decode_append(q_raw, k_new, v_new, q_stride, kv_stride, positions,
+                                             rope_table_cs, table_pos0, table_positions, theta,
+                                             append, rope_cur_cs);
+  rc = phase2_partial(q_raw, STAR_BF16, batch, 1, hq, hkv, d, k_pages, v_pages, STAR_BF16,
+                      num_pages, page_table, pages_per_seq, page_size, kv_len, max_kv_len, 0, out,
+                      lse, n_splits, workspace, &pp, &merged, (cudaStream_t)stream, &ap);
+  if (rc || merged) return rc;
+  return exchange_merge(boxes[rank], L, batch, 1, hq, hkv, d, out, STAR_F32, lse,
+                        (cudaStream_t)stream);
+}
+
+int star_decode_advance(int32_t* kv_len, int n_counters, int add, int64_t* positions,
+                        int n_positions, int inc, double* cur_cs, const double* rope_table_cs,
+                        int64_t table_pos0, int64_t table_positions, int d, double theta,
+                        void* stream) {
+  if (n_counters < 0 || n_positions < 0) return fail(STAR_ESHAPE, "decode_advance: negative count");
+  if ((n_counters > 0 && kv_len == nullptr) || (n_positions > 0 && positions == nullptr))
+    return fail(STAR_ESHAPE, "decode_advance: NULL counters / positions");
+  return decode_advance(kv_len, n_counters, add, positions, n_positions, inc, cur_cs,
+                        rope_table_cs, table_pos0, rope_table_cs ? table_positions : 0, d, theta,
+                        (cudaStream_t)stream);
 }
 
 int64_t star_exchange_box_bytes(int world, int64_t cap_rows, int cap_groups, int d) {

@@ -392,6 +392,53 @@ int kv_append(const void* qi, const void* ki, const void* vi, int dtype, int bat
   return STAR_OK;
 }
 
+// ------------------------------------------------------------------ decode advance
+// End of a fused decode step (star_phase2_decode appends without moving the counters, which
+// every K2 CTA reads): every layer's row counter += add and every position += inc, then the
+// cos/sin of the (new) positions into cur_cs [np][d/2] (from the decode-position table, else
+// the fp64 angle), so the next token's K2 reads them without a dependent position load.
+// One launch per token (inc = 0, add = 0: just fill cur_cs).
+__global__ void decode_advance_kernel(int32_t* __restrict__ kv_len, int n, int add,
+                                      int64_t* __restrict__ pos, int np, int inc,
+                                      double2* __restrict__ cur_cs, const double2* __restrict__ rtab,
+                                      int64_t pos0, int64_t ntab, int d, double theta) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int i = threadIdx.x; i < n; i += blockDim.x) kv_len[i] += add;
+  __shared__ int64_t ps[64];
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    const int64_t p = pos[i] + inc;
+    pos[i] = p;
+    if (i < 64) ps[i] = p;
+  }
+  if (cur_cs == nullptr) return;
+  __syncthreads();
+  const int half = d >> 1;
+  for (int idx = threadIdx.x; idx < np * half; idx += blockDim.x) {
+    const int b = idx / half, i = idx - b * half;
+    const int64_t p = b < 64 ? ps[b] : pos[b];
+    const int64_t tp = p - pos0;
+    if (rtab != nullptr && tp >= 0 && tp < ntab) {
+      cur_cs[idx] = rtab[tp * half + i];
+    } else {
+      double sn, c;
+      sincos((double)p * pow(theta, -2.0 * (double)i / (double)d), &sn, &c);
+      cur_cs[idx] = make_double2(c, sn);
+    }
+  }
+}
+
+int decode_advance(int32_t* kv_len, int n, int add, int64_t* pos, int np, int inc, void* cur_cs,
+                   const void* rtab, int64_t pos0, int64_t ntab, int d, double theta,
+                   cudaStream_t s) {
+  if (n == 0 && np == 0) return STAR_OK;
+  if (cur_cs != nullptr && (d < 2 || (d & 1) || !(theta > 0)))
+    return fail(STAR_ECONFIG, "decode_advance: bad head_dim / theta for the cos/sin refresh");
+  decode_advance_kernel<<<1, 256, 0, s>>>(kv_len, n, add, pos, np, inc, (double2*)cur_cs,
+                                          (const double2*)rtab, pos0, ntab, d, theta);
+  STAR_LAUNCH_CHECK("decode_advance");
+  return STAR_OK;
+}
+
 // ------------------------------------------------------------------ paged KV
 // Vector width W bytes; each thread moves one W-byte chunk of one (row, head).
 template <typename V>

@@ -73,6 +73,30 @@ struct PeerPush {
   uint64_t timeout_ns;
 };
 
+// Fused decode append for K2 (lq = 1, bf16): instead of a separate star_kv_append launch,
+// every K2 CTA rotates its q heads itself (RoPE at pos[b], cos/sin from the decode-position
+// table) and the CTA whose key range holds row kv_len[b] writes the new row's rotated k and
+// raw v into the paged cache right before its TMA reads that tile; K2 then attends over
+// kv_len[b] + add rows.  The row counter is NOT advanced here (every CTA reads it): the
+// decode step advances all layers' counters once per token (star_decode_advance).
+// on == 0: plain K2 (q already rotated, no append).
+struct DecodeAppend {
+  const void* q_raw;    // [batch][hq][d] pre-RoPE (row stride q_rs elements)
+  const void* k_new;    // [batch][hkv][d] pre-RoPE
+  const void* v_new;    // [batch][hkv][d]
+  int64_t q_rs, kv_rs;
+  const int64_t* pos;   // [batch] positions of the new rows
+  const void* rtab;     // double2 cos/sin table of positions [rtab_pos0, rtab_pos0 + rtab_n), or null
+  const void* cur_cs;   // double2 [batch][d/2] cos/sin at pos[b] (star_decode_advance keeps it
+                        // current), or null: read first, no dependent position load
+  int64_t rtab_pos0, rtab_n;
+  double theta;
+  void* kp;             // the K / V pools K2 streams (the new row is written there)
+  void* vp;
+  int on;               // rotate q from q_raw
+  int add;              // 1: append the row (write it, attend over kv_len + 1); 0: q only
+};
+
 // STAR_EXCHANGE_TIMEOUT_S (seconds, default 30), read once per process
 uint64_t spin_timeout_ns();
 

@@ -528,6 +528,7 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
   // pipe, MUFU ping-pong of the two heads; NQ == 2 runs the 12-warp layout (setmaxnreg gives
   // the softmax warpgroups 200 registers) with the MMA warp waiting without a suspend hint
   prm.seq = kDefaultSeq;
+  if (const char* sq = getenv("STAR_K1_SEQ")) prm.seq = atoi(sq);  // measurement knob
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const P1Params);
   KernT kern;
   int threads;
@@ -547,6 +548,8 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
     if constexpr (NQ == 2) {
       if (vv == 2) kern = phase1_tc_kernel<D, NQ, 0, 2, true, true, 1, false, 0>;
       if (vv == 3) kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0, true>;
+      if (vv == 4) kern = phase1_tc_kernel<D, NQ, 3, 2, true, true, 1, false, 0>;
+      if (vv == 5) kern = phase1_tc_kernel<D, NQ, 2, 2, true, true, 1, false, 0>;
     }
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);

@@ -410,7 +410,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
                const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
                const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
                float* lse, float* final_out, float* final_lse, int* counters, PeerPush pp,
-               int* merged, cudaStream_t s);
+               int* merged, cudaStream_t s, const DecodeAppend* dap);
 int push_partial(const float* out, const float* lse, int batch, int lq, int hq, int hkv, int d,
                  const PeerPush& pp, cudaStream_t s);
 bool phase2_qe_eligible(int qrows, int d, int page_size);
@@ -419,7 +419,8 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
                    const void* kp, const void* vp, int kv_dtype, int64_t num_pages,
                    const int32_t* table, int pps, int page_size, const int32_t* kv_len,
                    int64_t max_kv_len, int own_tail, float* out, float* lse, int n_splits,
-                   void* workspace, const PeerPush* push, int* merged, cudaStream_t s) {
+                   void* workspace, const PeerPush* push, int* merged, cudaStream_t s,
+                   const DecodeAppend* dap) {
   const PeerPush none{};
   if (merged != nullptr) *merged = 0;
   if (batch < 1 || lq < 1 || hq < 1 || hkv < 1 || hq % hkv)
@@ -477,8 +478,10 @@ int phase2_partial(const void* q, int q_dtype, int batch, int lq, int hq, int hk
     // into every rank's box (out / lse are then only the split workspace's neighbours)
     return phase2_mma(q, batch, lq, hq, hkv, d, kp, vp, num_pages, table, pps, page_size, kv_len,
                       own_tail, chunk, n_splits, po, pl, out, lse, counters,
-                      push ? *push : none, merged, s);
+                      push ? *push : none, merged, s, dap);
   }
+  if (dap != nullptr && dap->on)
+    return fail(STAR_ENOTSUP, "fused decode append needs the bf16 tensor-core path (page_size %% 64 == 0)");
 #define STAR_P2_D(TQ, TKV)                                                                    \
   switch (d) {                                                                                \
     case 128: rc = dispatch_qrb<TQ, TKV, 128>(QR, q, batch, lq, hq, hkv, kp, vp, table, pps,   \

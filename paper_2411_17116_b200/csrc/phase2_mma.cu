@@ -50,7 +50,8 @@ struct Smem {
   static constexpr int kTile = (D / 64) * kSlab;    // one K (or V) tile
   static constexpr int kStage = 2 * kTile;          // K + V
   static constexpr int kBarOff = STAGES * kStage;
-  static constexpr int kBytes = kBarOff + 2 * STAGES * 8 + 1024;
+  static constexpr int kQOff = kBarOff + 2 * STAGES * 8;  // fused decode: rotated q [16][D] bf16
+  static constexpr int kBytes = kQOff + 16 * D * 2 + 1024;
 };
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
@@ -342,6 +343,83 @@ __device__ void split_merge_words(int b, int kvh, int r_lo, int r_n, int lq, int
     exchange_merge_slice<D, NT>(b, kvh, r_lo, lq, hq, G, lo, hi, ep, final_out, final_lse, pp);
 }
 
+// ---- fused decode append helpers (DecodeAppend, exchange.cuh) ----
+// {cos, sin} of pair i at position p: the decode-position table entry when p is inside it,
+// else formed in place with the fp64 expression of rope_kernel (bit-identical either way)
+__device__ __noinline__ double2 rope_cs_slow(double theta, int64_t p, int i, int d) {
+  double sn, c;
+  sincos((double)p * pow(theta, -2.0 * (double)i / (double)d), &sn, &c);
+  return make_double2(c, sn);
+}
+__device__ __forceinline__ double2 rope_cs(const DecodeAppend& ap, int64_t p, int i, int d) {
+  const int64_t tp = p - ap.rtab_pos0;
+  if (ap.rtab != nullptr && tp >= 0 && tp < ap.rtab_n)
+    return reinterpret_cast<const double2*>(ap.rtab)[tp * (d >> 1) + i];
+  return rope_cs_slow(ap.theta, p, i, d);  // off the table: the fp64 angle (slow, rare)
+}
+// rotate one adjacent bf16 pair (packed in a 32-bit word) in fp64, round as the append kernel
+__device__ __forceinline__ uint32_t rope_pair_bf16(uint32_t w, double2 e) {
+  const double x0 = __bfloat162float(__ushort_as_bfloat16((unsigned short)(w & 0xFFFFu)));
+  const double x1 = __bfloat162float(__ushort_as_bfloat16((unsigned short)(w >> 16)));
+  const __nv_bfloat16 y0 = __float2bfloat16_rn(__double2float_rn(x0 * e.x - x1 * e.y));
+  const __nv_bfloat16 y1 = __float2bfloat16_rn(__double2float_rn(x0 * e.y + x1 * e.x));
+  return (uint32_t)__bfloat16_as_ushort(y0) | ((uint32_t)__bfloat16_as_ushort(y1) << 16);
+}
+// the new row of kv head kvh, prefetched by the consumer warp that owns it: rotated k and raw
+// v, lane l holding pairs l and l + 32 (the same rounding as kv_append_kernel)
+template <int D>
+struct NewRow {
+  uint32_t k[D / 64], v[D / 64];
+};
+template <int D>
+__device__ __forceinline__ NewRow<D> decode_new_row(const DecodeAppend& ap, int b, int kvh, int lane) {
+  const int64_t p = ap.cur_cs != nullptr ? 0 : ap.pos[b];
+  const uint32_t* kn = reinterpret_cast<const uint32_t*>(
+      reinterpret_cast<const __nv_bfloat16*>(ap.k_new) + (int64_t)b * ap.kv_rs + (int64_t)kvh * D);
+  const uint32_t* vn = reinterpret_cast<const uint32_t*>(
+      reinterpret_cast<const __nv_bfloat16*>(ap.v_new) + (int64_t)b * ap.kv_rs + (int64_t)kvh * D);
+  NewRow<D> nr;
+  double2 cs[D / 64];
+  uint32_t kw[D / 64];
+  const int64_t tp = p - ap.rtab_pos0;
+  const bool cur = ap.cur_cs != nullptr;
+  const bool tab = cur || (ap.rtab != nullptr && tp >= 0 && tp < ap.rtab_n);
+  const double2* src = cur ? reinterpret_cast<const double2*>(ap.cur_cs) + (int64_t)b * (D / 2)
+                           : reinterpret_cast<const double2*>(ap.rtab) + tp * (D / 2);
+#pragma unroll
+  for (int u = 0; u < D / 64; ++u) {
+    const int i = lane + 32 * u;  // pair index
+    kw[u] = kn[i];
+    nr.v[u] = vn[i];
+    if (tab) cs[u] = src[i];
+  }
+  if (!tab)
+#pragma unroll
+    for (int u = 0; u < D / 64; ++u) cs[u] = rope_cs_slow(ap.theta, p, lane + 32 * u, D);
+#pragma unroll
+  for (int u = 0; u < D / 64; ++u) nr.k[u] = rope_pair_bf16(kw[u], cs[u]);
+  return nr;
+}
+// write the new row into the cache (global, for the next tokens) and into row `r` of the
+// staged K / V tile (swizzled smem), so this launch attends over it without a round trip
+template <int D>
+__device__ __forceinline__ void decode_put_row(const NewRow<D>& nr, const DecodeAppend& ap,
+                                               int64_t pool_row, unsigned char* kb,
+                                               unsigned char* vb, int r, int lane) {
+  uint32_t* kd = reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(ap.kp) + pool_row * D);
+  uint32_t* vd = reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(ap.vp) + pool_row * D);
+#pragma unroll
+  for (int u = 0; u < D / 64; ++u) {
+    const int i = lane + 32 * u, c = 2 * i;  // pair i = elements c, c + 1
+    kd[i] = nr.k[u];
+    vd[i] = nr.v[u];
+    const int slab = c >> 6, chunk = (c & 63) >> 3;
+    const int off = slab * p2::TN * 128 + r * 128 + (((chunk ^ r) & 7) << 4) + (c & 7) * 2;
+    *reinterpret_cast<uint32_t*>(kb + off) = nr.k[u];
+    *reinterpret_cast<uint32_t*>(vb + off) = nr.v[u];
+  }
+}
+
 template <int D, bool KEYSPLIT>
 __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kernel(
     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -350,7 +428,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
     const int32_t* __restrict__ kv_len, int own_tail, int64_t chunk, float* __restrict__ out,
     float* __restrict__ lse, int64_t part_stride_rows, float scale_log2,
     float* __restrict__ final_out, float* __restrict__ final_lse, int* __restrict__ counters,
-    uint32_t* __restrict__ grp_epoch, const PeerPush pp) {
+    uint32_t* __restrict__ grp_epoch, const PeerPush pp, const DecodeAppend ap) {
   using namespace p2;
   using SM = Smem<D>;
   constexpr int NC = Cons<KEYSPLIT>::NC, NG = Cons<KEYSPLIT>::NG;
@@ -398,7 +476,8 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   // append that writes q's row and bumps kv_len): everything above overlapped that kernel;
   // nothing it writes is read before this point.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int64_t len = kv_len[b];
+  const int64_t base_len = kv_len[b];
+  const int64_t len = base_len + (ap.on ? ap.add : 0);
   const int64_t r1 = min(len, r0 + chunk);
   const int64_t tail0 = len - own_tail;
   const int ntiles = r1 > r0 ? (int)((r1 - r0 + TN - 1) / TN) : 0;
@@ -469,13 +548,40 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
       const __nv_bfloat16* qpB = nullptr;
       if (rA < QR) qpA = q + (((int64_t)b * lq + rA / G) * hq + kvh * G + rA % G) * D;
       if (rB < QR) qpB = q + (((int64_t)b * lq + rB / G) * hq + kvh * G + rB % G) * D;
+      if (KEYSPLIT && ap.on) {
+        // fused decode: the QR x D pre-RoPE rows of this group are rotated ONCE per CTA (one
+        // pair per consumer thread, the append kernel's fp64 rotation) into shared memory;
+        // every warp then takes its fragments from there.  lq == 1: row r is head kvh*G + r.
+        uint32_t* qs = reinterpret_cast<uint32_t*>(smem + SM::kQOff);
+        const __nv_bfloat16* qr = reinterpret_cast<const __nv_bfloat16*>(ap.q_raw) + (int64_t)b * ap.q_rs;
+        const int64_t p = ap.cur_cs != nullptr ? 0 : ap.pos[b];
+        for (int idx = threadIdx.x; idx < QR * (D / 2); idx += NC * 32) {
+          const int r = idx / (D / 2), i = idx % (D / 2);
+          const uint32_t raw = *reinterpret_cast<const uint32_t*>(qr + (int64_t)(kvh * G + r) * D + 2 * i);
+          const double2 cs = ap.cur_cs != nullptr
+                                 ? reinterpret_cast<const double2*>(ap.cur_cs)[(int64_t)b * (D / 2) + i]
+                                 : rope_cs(ap, p, i, D);
+          qs[idx] = rope_pair_bf16(raw, cs);
+        }
+        named_barrier_sync(1, NC * 32);
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        const int c = ks * 16 + t4 * 2;
-        qa[ks][0] = qpA ? *reinterpret_cast<const uint32_t*>(qpA + c) : 0u;
-        qa[ks][1] = qpB ? *reinterpret_cast<const uint32_t*>(qpB + c) : 0u;
-        qa[ks][2] = qpA ? *reinterpret_cast<const uint32_t*>(qpA + c + 8) : 0u;
-        qa[ks][3] = qpB ? *reinterpret_cast<const uint32_t*>(qpB + c + 8) : 0u;
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const int c = ks * 16 + t4 * 2;
+          const int rA2 = qbase + g4, rB2 = qbase + g4 + 8;
+          qa[ks][0] = rA2 < QR ? qs[(rA2 * D + c) >> 1] : 0u;
+          qa[ks][1] = rB2 < QR ? qs[(rB2 * D + c) >> 1] : 0u;
+          qa[ks][2] = rA2 < QR ? qs[(rA2 * D + c + 8) >> 1] : 0u;
+          qa[ks][3] = rB2 < QR ? qs[(rB2 * D + c + 8) >> 1] : 0u;
+        }
+      } else {
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const int c = ks * 16 + t4 * 2;
+          qa[ks][0] = qpA ? *reinterpret_cast<const uint32_t*>(qpA + c) : 0u;
+          qa[ks][1] = qpB ? *reinterpret_cast<const uint32_t*>(qpB + c) : 0u;
+          qa[ks][2] = qpA ? *reinterpret_cast<const uint32_t*>(qpA + c + 8) : 0u;
+          qa[ks][3] = qpB ? *reinterpret_cast<const uint32_t*>(qpB + c + 8) : 0u;
+        }
       }
     }
     // query row index (for the own-tail mask) of my two fragment rows
@@ -488,6 +594,18 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
     constexpr int KW = KEYSPLIT ? TN / 4 : TN;  // keys per warp per tile
     constexpr int NT_K = KW / 8;                 // n-tiles over keys
     const int kofs = KEYSPLIT ? wq4 * KW : 0;
+    // fused decode append: the warp whose keys hold row base_len (tile nt_new, key slot
+    // r_new) prefetches the new row now and patches it into the staged tile (and the cache)
+    int nt_new = -1, r_new = 0;
+    NewRow<D> nrow{};
+    if (KEYSPLIT && ap.on && ap.add && base_len >= r0 && base_len < r1) {
+      const int tn = (int)((base_len - r0) / TN), rr = (int)((base_len - r0) % TN);
+      if (tn % NG == grp && rr / KW == wq4) {
+        nt_new = tn;
+        r_new = rr;
+        nrow = decode_new_row<D>(ap, b, kvh, lane);
+      }
+    }
 
     for (int t = grp; t < ntiles; t += NG) {
       const int it = pass * ntiles + t;  // the producer's running tile index
@@ -512,6 +630,13 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
           __syncwarp();
         else
           named_barrier_sync(1, NC * 32);
+      }
+      if (KEYSPLIT && t == nt_new) {
+        const int64_t row = r0 + (int64_t)t * TN + r_new;
+        const int64_t pool_row = ((int64_t)table[row / page_size] * hkv + kvh) * page_size + row % page_size;
+        decode_put_row<D>(nrow, ap, pool_row, smem + st * SM::kStage, smem + st * SM::kStage + SM::kTile,
+                          r_new, lane);
+        __syncwarp();
       }
       // ---- S = Q K^T  (16 x KW) ----
       float sc[NT_K][4];
@@ -1158,9 +1283,18 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
                const void* vp, int64_t num_pages, const int32_t* table, int pps, int page_size,
                const int32_t* kv_len, int own_tail, int64_t chunk, int n_splits, float* out,
                float* lse, float* final_out, float* final_lse, int* counters, PeerPush pp,
-               int* merged, cudaStream_t s) {
+               int* merged, cudaStream_t s, const DecodeAppend* dap) {
   using namespace p2;
   if (merged != nullptr) *merged = 0;
+  DecodeAppend ap{};
+  if (dap != nullptr && dap->on) {
+    ap = *dap;
+    ap.kp = const_cast<void*>(kp);
+    ap.vp = const_cast<void*>(vp);
+    if (lq != 1 || (hq / hkv) > 16 || (d != 64 && d != 128))
+      return fail(STAR_ENOTSUP, "fused decode append: lq must be 1 and G <= 16 (got lq=%d G=%d)", lq,
+                  hq / hkv);
+  }
   pp.timeout_ns = spin_timeout_ns();
   auto fn = tensor_map_encoder();
   if (fn == nullptr) return fail(STAR_ECUDA, "cuTensorMapEncodeTiled unavailable");
@@ -1195,7 +1329,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   // word-mode fix-up (co-resident grid), else the mma.sync row blocks run
   bool use_qe = false;
   if (counters != nullptr && n_splits > 1 && !force_atomic) {
-    if (phase2_qe_eligible(QR, d, page_size) && (int64_t)n_splits * batch * hkv <= num_sms()) {
+    if (!ap.on && phase2_qe_eligible(QR, d, page_size) && (int64_t)n_splits * batch * hkv <= num_sms()) {
       use_qe = true;
       n_rb = 1;
       grid = dim3(n_splits, hkv, batch);
@@ -1203,7 +1337,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     } else if ((int64_t)n_splits * batch * hkv * n_rb <= num_sms()) {  // 1 CTA / SM
       grp_epoch = reinterpret_cast<uint32_t*>(counters) + kEpochOffsetWords;
     }
-  } else if (n_splits == 1 && phase2_qe_eligible(QR, d, page_size)) {
+  } else if (n_splits == 1 && !ap.on && phase2_qe_eligible(QR, d, page_size)) {
     // one split per (sequence, kv head): K2q writes the final partial, no fold (any grid)
     use_qe = true;
     n_rb = 1;
@@ -1301,7 +1435,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     cfg.numAttrs = na;                                                                          \
     e = cudaLaunchKernelEx(&cfg, kern, tk, tv, (const __nv_bfloat16*)q, lq, hq, hkv, table, pps, \
                            page_size, kv_len, own_tail, chunk, out, lse, part_rows, sl2,        \
-                           final_out, final_lse, counters, grp_epoch, pp);                      \
+                           final_out, final_lse, counters, grp_epoch, pp, ap);                  \
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 launch: %s", cudaGetErrorString(e));  \
   } while (0)
   if (d == 128) {

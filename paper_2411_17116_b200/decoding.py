@@ -50,6 +50,9 @@ class DeviceDecoder:
         self.graph: torch.cuda.CUDAGraph | None = None
         self._stepped = False
         self.launches_per_step = None
+        prime = getattr(attend_layer, "prime", None)
+        if prime is not None:
+            prime(self.pos)  # fused decode: cos/sin of the first position
 
     def _step(self) -> None:
         cfg = self.weights.config
@@ -62,7 +65,11 @@ class DeviceDecoder:
             att = self.attend_layer(li, q, k, v, self.pos)
             x = finish_layer(x, att.view(1, cfg.heads, cfg.head_dim), lw)
         self.logits.copy_(logits_from(self.weights, x)[-1])
-        self.pos += 1
+        finish = getattr(self.attend_layer, "finish", None)
+        if finish is not None:
+            finish(self.pos)  # fused decode: every layer's row counter and the position, 1 launch
+        else:
+            self.pos += 1
 
     def _capture(self) -> None:
         cur = torch.cuda.current_stream(self.device)
@@ -99,7 +106,7 @@ class DeviceDecoder:
 
 
 def paged_attend(pool, *, appends: bool, max_rows: int, theta: float, heads: int,
-                 exchange=None, group=None, rope_table=None) -> AttendLayer:
+                 exchange=None, group=None, rope_table=None, fused=None) -> AttendLayer:
     """Graph-safe phase-2 attention of one decode token against this rank's paged cache
     `pool` (the DeviceDecoder `attend_layer` of one rank; also the bench's 32-layer step).
 
@@ -111,15 +118,57 @@ def paged_attend(pool, *, appends: bool, max_rows: int, theta: float, heads: int
     one all-gather of the packed partial + K3; None without a group: K2 alone (one host).
     A rank with no rows pushes an empty partial (lse = -inf) so the merge stays collective.
     rope_table: ops.RopeTable of the decode positions (the append then reads cos/sin instead
-    of forming fp64 angles per token; bit-identical).
+    of forming fp64 angles per token; bit-identical), or an ops.DecodeRope (its table plus the
+    cos/sin at the current position, refreshed by .finish: the fused K2 then reads them with
+    no dependent position load).
+    fused: one launch per layer (ops.phase2_decode: RoPE + append inside K2; the returned
+    attend then has .finish(pos), which the decoder calls once per token to advance every
+    layer's row counter and the position).  Default: whenever the pool allows it (bf16,
+    page_size % 64 == 0, head_dim 64/128) and this rank holds rows.
     Returns the merged attention [1, H, hd] (fp32)."""
     H, hd = heads, pool.head_dim
     hkv = pool.hkv
     mine = max_rows > 0
+    # fused decode (star_phase2_decode): RoPE and the append inside K2, the row counters
+    # advanced once per token by attend.finish — one launch per layer instead of two
+    fused = (fused if fused is not None else
+             (pool.dtype == torch.bfloat16 and hd in (64, 128) and pool.page_size % 64 == 0
+              and H // hkv <= 16 and mine))
+
+    def attend_fused(li, q, k, v, pos):
+        qb = q.reshape(1, H, hd).to(pool.dtype)
+        kb = k.reshape(1, hkv, hd).to(pool.dtype) if appends else None
+        vb = v.reshape(1, hkv, hd).to(pool.dtype) if appends else None
+        kv = (pool.k[li], pool.v[li], pool.page_table.view(1, -1), pool.kv_len_tensor(li))
+        if exchange is not None:
+            att, _ = exchange.decode_exchange(qb, kb, vb, pos, *kv, max_rows, theta, rope_table,
+                                              appends, workspace=pool.workspace)
+            return att.view(1, H, hd)
+        if group is None:
+            att, _ = ops.phase2_decode(qb, kb, vb, pos, *kv, max_rows, theta, rope_table, appends,
+                                       workspace=pool.workspace)
+            return att.view(1, H, hd)
+        from .dist import gather_merge
+
+        packed, o, s = ops.packed_partial(H, hd, q.device)
+        ops.phase2_decode(qb, kb, vb, pos, *kv, max_rows, theta, rope_table, appends,
+                          out=o.view(1, 1, H, hd), lse=s.view(1, 1, H), workspace=pool.workspace)
+        att, _ = gather_merge(o, s, group=group, packed=packed)
+        return att.view(1, H, hd)
+
+    rope = rope_table if isinstance(rope_table, ops.DecodeRope) else None
+    flat_table = rope_table.table if rope is not None else rope_table
+
+    def finish(pos):
+        ops.decode_advance(pool.kv_len_dev if appends else pool.kv_len_dev[:0], pos, rope=rope)
+
+    def prime(pos):
+        if rope is not None:
+            rope.prime(pos)
 
     def attend(li, q, k, v, pos):
         if appends:
-            qr = pool.append_rope(li, q, k, v, pos, theta, table=rope_table)
+            qr = pool.append_rope(li, q, k, v, pos, theta, table=flat_table)
         else:
             qr = ops.rope(q.to(pool.dtype).contiguous(), pos, theta)
         qb = qr.view(1, 1, H, hd)
@@ -147,4 +196,8 @@ def paged_attend(pool, *, appends: bool, max_rows: int, theta: float, heads: int
         att, _ = gather_merge(o, s, group=group, packed=packed)
         return att.view(1, H, hd)
 
+    if fused:
+        attend_fused.finish = finish
+        attend_fused.prime = prime
+        return attend_fused
     return attend

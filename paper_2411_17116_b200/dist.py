@@ -177,6 +177,18 @@ class PeerExchange:
                                    self.boxes, self.cap_rows, self.cap_groups, self.rank,
                                    own_tail, n_splits, workspace)
 
+    def decode_exchange(self, q, k, v, positions, k_pages, v_pages, page_table, kv_len,
+                        max_kv_len, theta, table=None, append=True, n_splits: int = 0,
+                        workspace=None):
+        """Fused decode step (RoPE + append inside K2) + push + merge of every rank's partial
+        (ops.phase2_decode_exchange).  Returns fp32 (out [B, 1, hq, d], lse [B, 1, hq])."""
+        from . import ops
+
+        return ops.phase2_decode_exchange(q, k, v, positions, k_pages, v_pages, page_table,
+                                          kv_len, max_kv_len, self.boxes, self.cap_rows,
+                                          self.cap_groups, self.rank, theta, table, append,
+                                          n_splits, workspace)
+
     def push(self, out, lse, batch, lq, hq, hkv) -> None:
         from . import ops
 
@@ -439,8 +451,10 @@ def decode_dist(sess: DistSession, n_tokens: int, group=None, graph: bool | None
         # every rank sizes its decoder for the same token budget
         budget = -(-max(n_tokens, 64) // 64) * 64
         # (paged_attend's group=None means one host: pass the process group explicitly)
-        table = (ops.RopeTable(sess.next_position, room, cfg.head_dim, cfg.rope_theta,
-                               sess.pool.device) if room else None)
+        # cos/sin of the token budget's positions on every rank: the query rank's append and
+        # every rank's in-kernel q rotation (fused decode) read it
+        table = ops.DecodeRope(sess.next_position, budget, cfg.head_dim, cfg.rope_theta, 1,
+                               sess.pool.device)
         attend = paged_attend(sess.pool, appends=rank == sess.q_rank,
                               max_rows=rows + room if rank in sess.nonempty else 0,
                               theta=cfg.rope_theta, heads=cfg.heads, exchange=sess.exchange,

@@ -127,6 +127,23 @@ class RopeTable:
                   _stream(self.cs.device))
 
 
+class DecodeRope:
+    """RoPE state of a fused decoder: the cos/sin table of its token budget's positions
+    (RopeTable) plus `cur` — fp64 [batch, d/2, 2] cos/sin at the CURRENT positions, which
+    decode_advance refreshes at the end of every token, so the next star_phase2_decode reads
+    them without a dependent position load."""
+
+    def __init__(self, pos0: int, n: int, d: int, theta: float, batch: int, device):
+        self.table = RopeTable(pos0, n, d, theta, device)
+        self.d, self.theta, self.batch = int(d), float(theta), int(batch)
+        self.cur = torch.zeros((self.batch, d // 2, 2), dtype=torch.float64, device=device)
+
+    def prime(self, positions: torch.Tensor) -> None:
+        """cur <- cos/sin at `positions` (before the first token; no counter moves)."""
+        decode_advance(positions.new_zeros(0, dtype=torch.int32), positions, add=0, rope=self,
+                       inc=0)
+
+
 def kv_append(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, positions: torch.Tensor,
               kv_len: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
               page_table: torch.Tensor, theta: float = 10000.0,
@@ -327,12 +344,16 @@ _default_ws: dict = {}
 
 
 def _phase2_args(q, k_pages, v_pages, page_table, kv_len, max_kv_len, own_tail, n_splits, out,
-                 lse, workspace):
-    """Validated argument tuple of star_phase2_partial[_push] (everything but the stream)."""
+                 lse, workspace, qshape=None):
+    """Validated argument tuple of star_phase2_partial[_push] (everything but the stream).
+    qshape: (B, lq, hq, d) of a q whose layout the caller validated (the fused decode's
+    strided pre-RoPE rows)."""
     _cuda(q, k_pages, v_pages, page_table, kv_len)
-    if q.dim() != 4 or not q.is_contiguous():
-        raise ShapeError("q must be a contiguous [batch, lq, hq, d] tensor")
-    B, lq, hq, d = q.shape
+    if qshape is None:
+        if q.dim() != 4 or not q.is_contiguous():
+            raise ShapeError("q must be a contiguous [batch, lq, hq, d] tensor")
+        qshape = tuple(q.shape)
+    B, lq, hq, d = qshape
     if k_pages.dim() != 4 or k_pages.shape != v_pages.shape:
         raise ShapeError("k/v pools must be [num_pages, hkv, page_size, d]")
     _, hkv, page_size, dk = k_pages.shape
@@ -382,6 +403,100 @@ def phase2_partial(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor
                                   n_splits, out, lse, workspace)
     _lib.call("star_phase2_partial", *args, _stream(q.device))
     return out, lse
+
+
+def _decode_args(q, k, v, positions, append, theta, table, k_pages, v_pages, page_table, kv_len,
+                 max_kv_len, n_splits, out, lse, workspace):
+    """Validated argument tuple of star_phase2_decode[_exchange] (everything but the stream)."""
+    _cuda(q, positions, k_pages, v_pages, page_table, kv_len)
+    if q.dim() != 3 or q.stride(2) != 1 or q.stride(1) != q.shape[2]:
+        raise ShapeError("q must be [batch, hq, d] with packed heads")
+    B, hq, d = q.shape
+    if append:
+        _cuda(k, v)
+        if k.dim() != 3 or tuple(v.shape) != tuple(k.shape) or v.stride() != k.stride():
+            raise ShapeError("k / v must be [batch, hkv, d] with one layout")
+        if k.stride(2) != 1 or k.stride(1) != k.shape[2]:
+            raise ShapeError("k / v heads must be packed")
+    if q.dtype != torch.bfloat16 or k_pages.dtype != torch.bfloat16 or (append and k.dtype != torch.bfloat16):
+        raise ConfigError("the fused decode step is bf16")
+    if positions.dtype != torch.int64 or positions.numel() != B:
+        raise ShapeError(f"{positions.numel()} positions for batch {B} (int64 required)")
+    cur = None
+    if isinstance(table, DecodeRope):
+        if table.batch != B:
+            raise ShapeError(f"DecodeRope holds {table.batch} sequences, batch is {B}")
+        cur, table = table.cur, table.table
+    if table is not None and (table.d != d or table.theta != float(theta)):
+        raise ConfigError("rope table was built for another head_dim / theta")
+    (pargs, out, lse) = _phase2_args(q, k_pages, v_pages, page_table, kv_len, max_kv_len, 0,
+                                     n_splits, out, lse, workspace, qshape=(B, 1, hq, d))
+    _, _, _, _, _, hkv, _, kp, vp, _, num_pages, pt, pps, page_size, kl, mk, _, o, l, ns, ws = pargs
+    args = (q.data_ptr(), k.data_ptr() if append else None, v.data_ptr() if append else None,
+            1 if append else 0, q.stride(0), k.stride(0) if append else hkv * d,
+            positions.contiguous().data_ptr(), float(theta),
+            table.cs.data_ptr() if table is not None else None,
+            table.pos0 if table is not None else 0, table.n if table is not None else 0,
+            cur.data_ptr() if cur is not None else None,
+            B, hq, hkv, d, kp, vp, num_pages, pt, pps, page_size, kl, mk, o, l, ns, ws)
+    return args, out, lse
+
+
+def phase2_decode(q: torch.Tensor, k: torch.Tensor | None, v: torch.Tensor | None,
+                  positions: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
+                  page_table: torch.Tensor, kv_len: torch.Tensor, max_kv_len: int,
+                  theta: float = 10000.0, table: "RopeTable | DecodeRope | None" = None,
+                  append: bool = True,
+                  n_splits: int = 0, out: torch.Tensor | None = None,
+                  lse: torch.Tensor | None = None, workspace: Phase2Workspace | None = None):
+    """Fused decode step of one layer (star_phase2_decode): RoPE of the token's PRE-RoPE q
+    [B, hq, d] inside K2 and, with append, its rotated k / raw v [B, hkv, d] written at row
+    kv_len[b] of each paged cache by the K2 CTA that streams that row — then attention over
+    kv_len[b] + 1 rows.  One launch instead of kv_append + phase2_partial, bit-identical to
+    them.  kv_len is NOT advanced (decode_advance once per token).
+    Returns fp32 (out [B, 1, hq, d], lse [B, 1, hq])."""
+    args, out, lse = _decode_args(q, k, v, positions, append, theta, table, k_pages, v_pages,
+                                  page_table, kv_len, max_kv_len, n_splits, out, lse, workspace)
+    _lib.call("star_phase2_decode", *args, _stream(q.device))
+    return out, lse
+
+
+def phase2_decode_exchange(q, k, v, positions, k_pages, v_pages, page_table, kv_len,
+                           max_kv_len, boxes: Sequence[int], cap_rows: int, cap_groups: int,
+                           rank: int, theta: float = 10000.0, table: RopeTable | None = None,
+                           append: bool = True, n_splits: int = 0,
+                           workspace: Phase2Workspace | None = None):
+    """phase2_decode with the fused peer exchange (phase2_exchange): returns the merged
+    fp32 (out [B, 1, hq, d], lse [B, 1, hq]) on every rank."""
+    args, out, lse = _decode_args(q, k, v, positions, append, theta, table, k_pages, v_pages,
+                                  page_table, kv_len, max_kv_len, n_splits, None, None, workspace)
+    _lib.call("star_phase2_decode_exchange", *args, _box_array(boxes), len(boxes), int(cap_rows),
+              int(cap_groups), int(rank), _stream(q.device))
+    return out, lse
+
+
+def decode_advance(kv_len: torch.Tensor, positions: torch.Tensor | None, add: int = 1,
+                   rope: DecodeRope | None = None, inc: int = 1) -> None:
+    """End of a fused decode token (star_decode_advance, one launch): every int32 counter in
+    kv_len += add, every int64 position += inc and, with `rope`, rope.cur <- cos/sin at the new
+    positions."""
+    _cuda(kv_len)
+    if kv_len.dtype != torch.int32 or not kv_len.is_contiguous():
+        raise ConfigError("kv_len must be contiguous int32")
+    if positions is not None:
+        _cuda(positions)
+        if positions.dtype != torch.int64 or not positions.is_contiguous():
+            raise ConfigError("positions must be contiguous int64")
+    if rope is not None and (positions is None or positions.numel() != rope.batch):
+        raise ShapeError("rope refresh needs one position per sequence")
+    tab = rope.table if rope is not None else None
+    _lib.call("star_decode_advance", kv_len.data_ptr(), kv_len.numel(), int(add),
+              positions.data_ptr() if positions is not None else None,
+              positions.numel() if positions is not None else 0, int(inc),
+              rope.cur.data_ptr() if rope is not None else None,
+              tab.cs.data_ptr() if tab is not None else None, tab.pos0 if tab is not None else 0,
+              tab.n if tab is not None else 0, rope.d if rope is not None else 0,
+              rope.theta if rope is not None else 0.0, _stream(kv_len.device))
 
 
 # ---------------------------------------------------------------- peer exchange (fused C1)

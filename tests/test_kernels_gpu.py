@@ -448,3 +448,108 @@ def test_kv_append_equals_rope_and_page_write(ops, dtype, B, rows):
     assert torch.equal(kp, kp2) and torch.equal(vp, vp2)
     assert torch.equal(kp_t, kp2) and torch.equal(vp_t, vp2)
     assert kv_len.tolist() == [s + rows for s in start] == kv_len_t.tolist()
+
+
+@pytest.mark.parametrize("B,hq,hkv,d,starts", [
+    (1, 32, 8, 128, [16383]),          # Llama-8B heads, the new row ends a 64-key tile
+    (1, 32, 8, 128, [16384]),          # the new row opens a new page / tile
+    (3, 8, 2, 128, [37, 4095, 200]),   # batch, ragged lengths
+    (2, 8, 8, 64, [129, 0]),           # MHA, head_dim 64, an empty cache (first row)
+])
+@pytest.mark.parametrize("use_table", ["table", "none", "cur"])
+def test_phase2_decode_equals_append_then_k2(ops, B, hq, hkv, d, starts, use_table):
+    """star_phase2_decode (RoPE + append inside K2, one launch) is BIT-IDENTICAL to
+    star_kv_append followed by star_phase2_partial: same pages written, same (out, lse); the
+    counters are untouched until star_decode_advance, which adds 1 to each and 1 to each
+    position.  append=False (a rank that only rotates q) equals rope + K2."""
+    page = 128
+    maxk = max(starts) + 64
+    pps = -(-maxk // page)
+    torch.manual_seed(7)
+    q = torch.randn(B, hq, d).bfloat16().cuda()
+    k = torch.randn(B, hkv, d).bfloat16().cuda()
+    v = torch.randn(B, hkv, d).bfloat16().cuda()
+    pos = torch.tensor([s + 11 for s in starts], dtype=torch.int64).cuda()
+    table = torch.randperm(B * pps).to(torch.int32).view(B, pps).cuda()
+    kp = ops.prng_fill((B * pps, hkv, page, d), 3, 1, 1.0, torch.bfloat16, torch.device("cuda"))
+    vp = ops.prng_fill((B * pps, hkv, page, d), 4, 1, 1.0, torch.bfloat16, torch.device("cuda"))
+    tab = ops.RopeTable(min(starts) + 11, maxk, d, 10000.0, "cuda") if use_table == "table" else None
+    rope = None
+    if use_table == "cur":  # DecodeRope: cos/sin at the current positions, primed on the device
+        rope = ops.DecodeRope(min(starts) + 11, maxk, d, 10000.0, B, "cuda")
+        rope.prime(pos)
+        tab = rope.table
+    # reference: append kernel + K2
+    kp_r, vp_r = kp.clone(), vp.clone()
+    kl_r = torch.tensor(starts, dtype=torch.int32).cuda()
+    qr = ops.kv_append(q.view(B, hq, d), k, v, pos, kl_r, kp_r, vp_r, table, table=tab)
+    o_r, l_r = ops.phase2_partial(qr.view(B, 1, hq, d), kp_r, vp_r, table, kl_r, maxk)
+    # fused
+    kl = torch.tensor(starts, dtype=torch.int32).cuda()
+    o, l = ops.phase2_decode(q, k, v, pos, kp, vp, table, kl, maxk, table=rope or tab)
+    torch.cuda.synchronize()
+    assert torch.equal(kp, kp_r) and torch.equal(vp, vp_r)
+    assert torch.equal(o, o_r) and torch.equal(l, l_r)
+    assert kl.tolist() == starts
+    pos2 = pos.clone()
+    ops.decode_advance(kl, pos2, rope=rope)
+    torch.cuda.synchronize()
+    assert kl.tolist() == [s + 1 for s in starts] and torch.equal(pos2, pos + 1)
+    if rope is not None:  # cur now holds the table rows of the advanced positions
+        for b in range(B):
+            assert torch.equal(rope.cur[b], rope.table.cs[int(pos2[b]) - rope.table.pos0])
+    # rotate-only (no append) == rope + K2 over the unchanged cache
+    kl0 = torch.tensor(starts, dtype=torch.int32).cuda()
+    if rope is not None:
+        rope.prime(pos)
+    o2, l2 = ops.phase2_decode(q, None, None, pos, kp, vp, table, kl0, maxk, table=rope or tab,
+                               append=False)
+    o3, l3 = ops.phase2_partial(ops.rope(q, pos).view(B, 1, hq, d), kp, vp, table, kl0, maxk)
+    torch.cuda.synchronize()
+    assert torch.equal(o2, o3) and torch.equal(l2, l3)
+
+
+def test_phase2_decode_exchange_equals_unfused(ops):
+    """The fused decode step through the one-kernel peer exchange (2 ranks' boxes on one GPU,
+    one stream per rank, grids small enough to be co-resident as on separate GPUs) equals the
+    fused decode partials merged by K3, bit for bit; rank 1 (the query rank) appends."""
+    from paper_2411_17116_b200.dist import local_peer_exchanges
+
+    B, hq, hkv, d, page, splits = 1, 32, 8, 128, 128, 4
+    rows = [5000, 7000]
+    maxk = max(rows) + 64
+    pps = -(-maxk // page)
+    dev = torch.device("cuda")
+    torch.manual_seed(3)
+    q = torch.randn(B, hq, d).bfloat16().cuda()
+    k = torch.randn(B, hkv, d).bfloat16().cuda()
+    v = torch.randn(B, hkv, d).bfloat16().cuda()
+    pos = torch.tensor([rows[1] + 3], dtype=torch.int64).cuda()
+    tab = ops.RopeTable(int(pos[0]), 8, d, 10000.0, "cuda")
+    pools = [(ops.prng_fill((pps, hkv, page, d), 10 + r, 1, 1.0, torch.bfloat16, dev),
+              ops.prng_fill((pps, hkv, page, d), 20 + r, 1, 1.0, torch.bfloat16, dev),
+              torch.arange(pps, dtype=torch.int32, device=dev).view(1, -1)) for r in range(2)]
+    refs = []
+    for r in range(2):
+        kp, vp, tb = pools[r]
+        kl = torch.tensor([rows[r]], dtype=torch.int32, device=dev)
+        refs.append(ops.phase2_decode(q, k, v, pos, kp.clone(), vp.clone(), tb, kl, maxk,
+                                      table=tab, append=r == 1, n_splits=splits))
+    exs = local_peer_exchanges(2, hq, hkv, d, dev)
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    kls = [torch.tensor([rows[r]], dtype=torch.int32, device=dev) for r in range(2)]
+    torch.cuda.synchronize()
+    outs = [None, None]
+    for r in range(2):
+        kp, vp, tb = pools[r]
+        with torch.cuda.stream(streams[r]):
+            outs[r] = exs[r].decode_exchange(q, k, v, pos, kp, vp, tb, kls[r], maxk, 10000.0, tab,
+                                             append=r == 1, n_splits=splits,
+                                             workspace=ops.Phase2Workspace())
+    torch.cuda.synchronize()
+    o_ref, l_ref = ops.merge(torch.stack([refs[0][0].view(-1, d), refs[1][0].view(-1, d)]),
+                             torch.stack([refs[0][1].view(-1), refs[1][1].view(-1)]))
+    torch.cuda.synchronize()
+    for o, l in outs:
+        assert torch.equal(o.view(-1, d), o_ref.view(-1, d))
+        assert torch.equal(l.view(-1), l_ref.view(-1))

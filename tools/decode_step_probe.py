@@ -71,8 +71,24 @@ def main():
             app_k2()
             pos.add_(1)
 
+        drope = ops.DecodeRope(rows, 4096, d, 10000.0, 1, dev)
+        drope.prime(pos)
+
+        def fused():
+            ops.phase2_decode(q, kn, vn, pos, kp, vp, table, kv_len, maxk, table=rtab, workspace=ws)
+
+        def fused_cur():
+            ops.phase2_decode(q, kn, vn, pos, kp, vp, table, kv_len, maxk, table=drope,
+                              workspace=ws)
+
+        def fused_step():
+            fused_cur()
+            ops.decode_advance(kv_len, pos, rope=drope)
+
         out = {}
-        for name, fn in (("k2", k2), ("append", append), ("app+k2", app_k2), ("step", step)):
+        for name, fn in (("k2", k2), ("append", append), ("app+k2", app_k2), ("step", step),
+                         ("fused", fused), ("fused_cur", fused_cur),
+                         ("fused+advance", fused_step)):
             kv_len.fill_(rows)
             out[name] = graph_us(fn)
         res[rows] = out

@@ -27,6 +27,7 @@ p.add_argument("--rows", type=int, default=16384)
 p.add_argument("--batch", type=int, default=1)
 p.add_argument("--splits", type=int, default=0)
 p.add_argument("--exchange", action="store_true", help="fused star_phase2_exchange (self-loop)")
+p.add_argument("--decode", action="store_true", help="fused decode step (star_phase2_decode)")
 a = p.parse_args()
 dev = torch.device("cuda", 0)
 hq, hkv, d, page = 32, 8, 128, 128
@@ -42,8 +43,16 @@ ncta = splits * hkv * a.batch
 if a.exchange:
     from paper_2411_17116_b200 import dist as D
     ex = D.local_peer_exchanges(1, hq * a.batch, hkv * a.batch, d, dev)[0]
+kn = ops.prng_fill((a.batch, hkv, d), 8, 1, 1.0, torch.bfloat16, dev)
+vn = ops.prng_fill((a.batch, hkv, d), 9, 1, 1.0, torch.bfloat16, dev)
+pos = torch.full((a.batch,), a.rows - 1, dtype=torch.int64, device=dev)
+rtab = ops.RopeTable(a.rows - 1, 8, d, 10000.0, dev)
 for _ in range(20):
-    if a.exchange:
+    if a.decode:
+        kv_len.fill_(a.rows - 1)
+        ops.phase2_decode(q.view(a.batch, hq, d), kn, vn, pos, kp, vp, table, kv_len, a.rows,
+                          table=rtab, n_splits=splits, workspace=ws)
+    elif a.exchange:
         ex.exchange(q, kp, vp, table, kv_len, a.rows, n_splits=splits, workspace=ws)
     else:
         ops.phase2_partial(q, kp, vp, table, kv_len, a.rows, n_splits=splits, workspace=ws)
