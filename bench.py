@@ -782,10 +782,18 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
             if gib > cap_gib:
                 continue
             pps = -(-(rows + n_tokens) // page)
-            kp = torch.empty((B * pps, hkv, page, d), dtype=torch.bfloat16, device=dev)
-            vp = torch.empty_like(kp)
-            ops.prng_fill(None, 21, out=kp.view(-1))
-            ops.prng_fill(None, 22, out=vp.view(-1))
+            # L2-cold: a cache smaller than 512 MiB is replicated (one copy per launch, cycled)
+            # so every launch streams its K/V from HBM, as distinct layers do
+            cache_b = B * pps * page * hkv * d * 2 * 2
+            n_c = 1 if cache_b >= 512 * 2 ** 20 else -(-512 * 2 ** 20 // cache_b)
+            lpt = max(LPT, n_c)
+            caches = []
+            for ci in range(n_c):
+                kp = torch.empty((B * pps, hkv, page, d), dtype=torch.bfloat16, device=dev)
+                vp = torch.empty_like(kp)
+                ops.prng_fill(None, 21 + 2 * ci, out=kp.view(-1))
+                ops.prng_fill(None, 22 + 2 * ci, out=vp.view(-1))
+                caches.append((kp, vp))
             table = torch.arange(B * pps, dtype=torch.int32, device=dev).view(B, pps)
             q = ops.prng_fill((B, 1, hq, d), 23, 1, 1.0, torch.bfloat16, dev)
             kn = ops.prng_fill((B, hkv, d), 24, 1, 1.0, torch.bfloat16, dev)
@@ -801,7 +809,8 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
                 # LPT layers' worth of fused decode launches over this cache (each attends
                 # over kv_len + 1 rows and writes the token's row), then the once-per-token
                 # counter / position advance — per layer = step / LPT, as in a model step
-                for _ in range(LPT):
+                for li in range(lpt):
+                    kp, vp = caches[li % n_c]
                     ops.phase2_decode(q.view(B, hq, d), kn, vn, pos, kp, vp, table, kv_len, maxk,
                                       table=rtab, workspace=ws)
                 ops.decode_advance(kv_len, pos, rope=rtab)
@@ -823,10 +832,10 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
                 g.replay()
             e1.record()
             torch.cuda.synchronize(dev)
-            us = e0.elapsed_time(e1) / n_tokens / LPT * 1e3
+            us = e0.elapsed_time(e1) / n_tokens / lpt * 1e3
             nbytes = B * (rows + n_tokens / 2) * hkv * d * 2 * 2  # mean cache over the 64 tokens
             kern[(B, rows)] = (us, nbytes / us / 1e3)
-            del kp, vp, g
+            del caches, g
             torch.cuda.empty_cache()
     merge_us = {}
     for B in Bs:
@@ -866,10 +875,12 @@ def decode_sweep(dev, hq, hkv, d, hbm_peak, n_tokens=64, cap_gib=64.0):
                             "frac_of_measured_hbm": k[1] / hbm_peak,
                             "merge_us": merge_us.get((B, G))})
     return {"points": out, "tokens": n_tokens,
-            "timing": "per (B, S/G): CUDA graph of 8 star_phase2_decode launches (RoPE + append "
+            "timing": "per (B, S/G): CUDA graph of max(8, copies) star_phase2_decode launches (RoPE + append "
                       "of the B new rows inside K2 over the B paged caches, one per layer) + one "
                       "star_decode_advance, replayed for 64 generated tokens; value per layer = "
-                      "graph / 8; merge_us = K3 over G partials (graph-replayed launches)"}
+                      "graph / launches; every launch reads its K/V from HBM (caches under 512 MiB are "
+                      "replicated and cycled, L2-cold); merge_us = K3 over G partials "
+                      "(graph-replayed launches)"}
 
 
 def cfg1_session(dev):
