@@ -1,8 +1,8 @@
 """Small launches of every product kernel for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): K1 (tcgen05, both head dims, dedup, query range), the fp32 check
 kernels, K2 decode (word-mode split fold), K2q query encode, the fused one-kernel peer
-exchange and the K2-push + K3x pair (local boxes), K3 merge, the decode append, RoPE,
-page write/read.  usage: compute-sanitizer --tool X python tools/sanitize_cases.py"""
+exchange and the K2-push + K3x pair (local boxes), K3 merge, the decode append, the fused
+decode step (star_phase2_decode[_exchange], star_decode_advance), RoPE, page write/read.  usage: compute-sanitizer --tool X python tools/sanitize_cases.py"""
 import os
 import sys
 
@@ -67,6 +67,16 @@ def main():
         exs[r].merge(1, 1, hq, hkv)
     o, s = ops.phase2_partial(q1, kp, vp, table.view(1, -1), kv_len, n)
     ops.merge(torch.stack([o.view(hq, d)] * 3), torch.stack([s.view(hq)] * 3))
+    # fused decode (RoPE + append inside K2), with the current-position cos/sin, the counter
+    # advance, and the fused decode through the one-kernel exchange (1 rank)
+    posn = torch.tensor([n], dtype=torch.int64, device=dev)
+    rope = ops.DecodeRope(n, 8, d, 10000.0, 1, dev)
+    rope.prime(posn)
+    ops.phase2_decode(qn, kn, kn, posn, kp, vp, table.view(1, -1), kv_len, n + 1, table=rope)
+    ops.phase2_decode(qn, None, None, posn, kp, vp, table.view(1, -1), kv_len, n + 1, table=rope,
+                      append=False)
+    ex1.decode_exchange(qn, kn, kn, posn, kp, vp, table.view(1, -1), kv_len, n + 1, 10000.0, rope)
+    ops.decode_advance(kv_len, posn, rope=rope)
     torch.cuda.synchronize()
     print("sanitize cases done")
 
