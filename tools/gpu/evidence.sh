@@ -1,10 +1,11 @@
 # round-2 evidence: compute-sanitizer over every product kernel, ncu launch list + full captures
+TAG=${1:-r02}
 mkdir -p gpurun_out
 export STAR_EXCHANGE_TIMEOUT_S=600
 for tool in memcheck racecheck synccheck initcheck; do
   timeout -s KILL 900 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_cases.py \
-    > gpurun_out/r02b_sanitize_${tool}.log 2>&1
-  echo "exit=$?" >> gpurun_out/r02b_sanitize_${tool}.log
+    > gpurun_out/${TAG}_sanitize_${tool}.log 2>&1
+  echo "exit=$?" >> gpurun_out/${TAG}_sanitize_${tool}.log
 done
 unset STAR_EXCHANGE_TIMEOUT_S
-bash tools_profile.sh r02b > gpurun_out/r02b_profile.log 2>&1
+bash tools_profile.sh ${TAG} > gpurun_out/${TAG}_profile.log 2>&1
