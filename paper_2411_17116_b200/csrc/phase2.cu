@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kP2Threads, 4) phase2_partial_kernel(
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        __syncwarp();  // every lane has read mrow_s[rr] before lane 0 rewrites it
         if (lane == 0) {
           const float a = (m_prev == -INFINITY) ? 0.f : expf(m_prev - m_new);
           alpha_s[rr] = a;

@@ -44,13 +44,17 @@ struct Cons {
   static constexpr int kThreads = (NC + 1) * 32;
 };
 
-template <int D>
+// ST stages of K + V (6: 192 KB in flight per SM).  ST must be EVEN in the decode mode: its two
+// consumer groups take alternate tiles, and with an odd ring a group can reach a stage two
+// phases ahead of the other's pending tile, where the mbarrier parity wait aliases (a 3-stage
+// ring, tried for two CTAs per SM, failed the bit-exactness tests for that reason).
+template <int D, int ST = STAGES>
 struct Smem {
   static constexpr int kSlab = TN * 128;            // [TN rows x 64 bf16] swizzled
   static constexpr int kTile = (D / 64) * kSlab;    // one K (or V) tile
   static constexpr int kStage = 2 * kTile;          // K + V
-  static constexpr int kBarOff = STAGES * kStage;
-  static constexpr int kQOff = kBarOff + 2 * STAGES * 8;  // fused decode: rotated q [16][D] bf16
+  static constexpr int kBarOff = ST * kStage;
+  static constexpr int kQOff = kBarOff + 2 * ST * 8;  // fused decode: rotated q [16][D] bf16
   static constexpr int kBytes = kQOff + 16 * D * 2 + 1024;
 };
 
@@ -420,7 +424,7 @@ __device__ __forceinline__ void decode_put_row(const NewRow<D>& nr, const Decode
   }
 }
 
-template <int D, bool KEYSPLIT>
+template <int D, bool KEYSPLIT, int ST = p2::STAGES>
 __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kernel(
     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
     const __nv_bfloat16* __restrict__ q, int lq, int hq, int hkv,
@@ -430,14 +434,15 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
     float* __restrict__ final_out, float* __restrict__ final_lse, int* __restrict__ counters,
     uint32_t* __restrict__ grp_epoch, const PeerPush pp, const DecodeAppend ap) {
   using namespace p2;
-  using SM = Smem<D>;
+  using SM = Smem<D, ST>;
+  static_assert(!KEYSPLIT || ST % 2 == 0, "decode mode: the ring depth must be even (see Smem)");
   constexpr int NC = Cons<KEYSPLIT>::NC, NG = Cons<KEYSPLIT>::NG;
   constexpr int NT_D = D / 8;  // n-tiles over head dim (P.V output)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kBarOff);
-  uint64_t* empty = full + STAGES;
+  uint64_t* empty = full + ST;
 
   // row mode (G*lq > 16 query rows, e.g. a 32-token query encode) splits the group's rows
   // into 64-row blocks along grid.y, so every K/V tile is streamed once per split (the row
@@ -461,7 +466,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   const int n_pass = 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 4);  // one group of four consumer warps per tile
     }
@@ -508,8 +513,8 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
         for (int u = 0; u < cnt; ++u, ++it) {
           const int prow = __shfl_sync(0xffffffffu, cur, u);
           if (lane == 0) {
-            const int st = it % STAGES;
-            if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) + 1) & 1);
+            const int st = it % ST;
+            if (it >= ST) mbar_wait(&empty[st], ((it / ST) + 1) & 1);
             unsigned char* kb = smem + st * SM::kStage;
             mbar_expect_tx(&full[st], SM::kStage);
 #pragma unroll
@@ -609,8 +614,8 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
 
     for (int t = grp; t < ntiles; t += NG) {
       const int it = pass * ntiles + t;  // the producer's running tile index
-      const int st = it % STAGES;
-      mbar_wait(&full[st], (it / STAGES) & 1);
+      const int st = it % ST;
+      mbar_wait(&full[st], (it / ST) & 1);
       K2_TR(it == 0 && threadIdx.x == 0, 1);
       const uint32_t kbase = smem_u32(smem + st * SM::kStage);
       const uint32_t vbase = kbase + SM::kTile;
@@ -895,7 +900,9 @@ __device__ __forceinline__ float row_max_half(const uint32_t (&sv)[2][32], int l
 // half's own S columns: every 16 keys take 16 columns, hi (8 columns) then lo (8 columns),
 // so a 32-key chunk is ONE 32-column tcgen05.st; P.V reads hi of keys [16g, 16g+16) at
 // column 16g and lo at 16g + 8.  Returns the sum of hi + lo.
-template <bool DIAG>
+// FS: row sums as fp32 FADD2 over the unrounded p (half an instruction per element) instead of
+// two FHADD.BF16 (hi and lo parts) per element
+template <bool DIAG, bool FS>
 __device__ __forceinline__ float exp_pack_hilo_half(const uint32_t (&sv)[2][32], uint32_t p_base,
                                                     int lim, int colbase, float sl2, float m) {
   float2 rsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -925,14 +932,19 @@ __device__ __forceinline__ float exp_pack_hilo_half(const uint32_t (&sv)[2][32],
       w[g * 16 + k] = wh;
       w[g * 16 + 8 + k] = wl;
       float2& acc = rsum[(e >> 1) & 1];
-      acc_bf16x2(acc.x, acc.y, wh);
-      acc_bf16x2(acc.x, acc.y, wl);
+      if (FS) {
+        acc = fadd2(acc, make_float2(p0, p1));
+      } else {
+        acc_bf16x2(acc.x, acc.y, wh);
+        acc_bf16x2(acc.x, acc.y, wl);
+      }
     }
     tmem_st32(p_base + c * 32, w);
   }
   return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
 }
 
+template <bool FS>
 __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
     const __grid_constant__ CUtensorMap tm_v, int lq, int hq, int hkv,
@@ -1077,7 +1089,8 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
           umma_bf16_ss_warp(tbase + (t % kSBuf) * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
         }
         umma_commit_warp(&s_full[t % kSBuf]);
-        umma_commit_warp(&k_empty[st]);
+        // release a stage only if the producer will refill it (commit only what is waited)
+        if (t + KST < ntiles) umma_commit_warp(&k_empty[st]);
       };
       mbar_wait(q_full, 0);
       for (int t = 0; t < kSBuf && t < ntiles; ++t) issue_s(t);
@@ -1097,11 +1110,17 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
                          (j > 0 || h > 0 || kk > 0) ? 1u : 0u);
         }
         K2Q_TR(true, j, 6);
-        umma_commit_warp(&o_done[j % kSBuf]);
+        if (j + 1 < ntiles) umma_commit_warp(&o_done[j % kSBuf]);  // waited by a rescale of j+1
         if (j == ntiles - 1) umma_commit_warp(o_last);
-        umma_commit_warp(&v_empty[vs]);
+        if (j + VST < ntiles) umma_commit_warp(&v_empty[vs]);
         if (j + kSBuf < ntiles) issue_s(j + kSBuf);
         K2Q_TR(true, j, 7);
+      }
+      // consume the last phase of every o_done barrier (a rescale waits on them only when
+      // the running max jumps): no commit arrival is left unobserved when the CTA exits
+      for (int i = 0; i < kSBuf; ++i) {
+        const int n_i = ntiles - 1 > i ? (ntiles - 1 - i + kSBuf - 1) / kSBuf : 0;
+        if (n_i > 0) mbar_wait(&o_done[i], (n_i - 1) & 1);
       }
     }
   } else {
@@ -1155,8 +1174,8 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       if (pad || last_rel < 0) m_use = 0.f;
       // P of keys [64h, 64h+64) over this half's own S columns [64h, 64h+64)
       const uint32_t p_base = s_tm + hf * 64;
-      const float rs = masked ? exp_pack_hilo_half<true>(sv, p_base, lim, hf * 64, sl2, m_use)
-                              : exp_pack_hilo_half<false>(sv, p_base, lim, hf * 64, sl2, m_use);
+      const float rs = masked ? exp_pack_hilo_half<true, FS>(sv, p_base, lim, hf * 64, sl2, m_use)
+                              : exp_pack_hilo_half<false, FS>(sv, p_base, lim, hf * 64, sl2, m_use);
       K2Q_TR(threadIdx.x == 0, j, 3);
       if (r1 - base < BN) {
         // keys past the split end: their V rows may hold stale (even non-finite) data and
@@ -1380,7 +1399,13 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
            qestr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return fail(STAR_ECUDA, "phase2 query encode: Q tensor map encode failed");
-    cudaError_t e = cudaFuncSetAttribute(phase2_qe_kernel,
+    static int fs = -1;  // STAR_K2Q_SUM=0: the round-1 FHADD.BF16 row sums (measurement knob)
+    if (fs < 0) {
+      const char* ev = getenv("STAR_K2Q_SUM");
+      fs = (ev != nullptr && ev[0] == '0') ? 0 : 1;
+    }
+    auto qek = fs ? phase2_qe_kernel<true> : phase2_qe_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(qek,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, p2q::kSmem);
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 qe smem attr: %s", cudaGetErrorString(e));
     cudaLaunchAttribute attr[2];
@@ -1400,7 +1425,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    e = cudaLaunchKernelEx(&cfg, phase2_qe_kernel, tq, tk, tv, lq, hq, hkv, table, pps, page_size,
+    e = cudaLaunchKernelEx(&cfg, qek, tq, tk, tv, lq, hq, hkv, table, pps, page_size,
                            kv_len, own_tail, chunk, reinterpret_cast<uint2*>(out), part_rows, sl2,
                            final_out, final_lse, grp_epoch, pp);
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 qe launch: %s", cudaGetErrorString(e));
@@ -1410,10 +1435,10 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   // Word mode spins on other CTAs of the grid, so it is launched COOPERATIVELY: the driver
   // guarantees every CTA co-resident (also against kernels on other streams), and refuses the
   // launch instead of deadlocking if the grid cannot fit.
-#define STAR_P2M(DD, KS)                                                                        \
+#define STAR_P2M_ST(DD, KS, SST)                                                                \
   do {                                                                                          \
-    auto kern = phase2_mma_kernel<DD, KS>;                                                      \
-    const int bytes = Smem<DD>::kBytes;                                                         \
+    auto kern = phase2_mma_kernel<DD, KS, SST>;                                                 \
+    const int bytes = Smem<DD, SST>::kBytes;                                                    \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \
     cudaLaunchAttribute attr[2];                                                                \
@@ -1438,6 +1463,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
                            final_out, final_lse, counters, grp_epoch, pp, ap);                  \
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 launch: %s", cudaGetErrorString(e));  \
   } while (0)
+#define STAR_P2M(DD, KS) STAR_P2M_ST(DD, KS, STAGES)
   if (d == 128) {
     if (keysplit) STAR_P2M(128, true); else STAR_P2M(128, false);
   } else if (d == 64) {
@@ -1446,6 +1472,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     return fail(STAR_ENOTSUP, "phase2 bf16 path needs head_dim 64 or 128");
   }
 #undef STAR_P2M
+#undef STAR_P2M_ST
   STAR_LAUNCH_CHECK("phase2_mma");
   return STAR_OK;
 }

@@ -2,7 +2,12 @@
 synccheck / initcheck): K1 (tcgen05, both head dims, dedup, query range), the fp32 check
 kernels, K2 decode (word-mode split fold), K2q query encode, the fused one-kernel peer
 exchange and the K2-push + K3x pair (local boxes), K3 merge, the decode append, the fused
-decode step (star_phase2_decode[_exchange], star_decode_advance), RoPE, page write/read.  usage: compute-sanitizer --tool X python tools/sanitize_cases.py"""
+decode step (star_phase2_decode[_exchange], star_decode_advance), RoPE, page write/read.  usage: compute-sanitizer --tool X python tools/sanitize_cases.py [--serial]
+
+--serial: every split-KV launch with ONE split per (sequence, kv head), so no CTA spin-waits on
+another (racecheck / synccheck run CTAs one at a time, under which the co-resident word-mode
+fold and the one-kernel exchange cannot make progress); the exchanges then take the
+K2-push + K3x form."""
 import os
 import sys
 
@@ -15,6 +20,8 @@ from paper_2411_17116_b200 import ops  # noqa: E402
 
 
 def main():
+    serial = "--serial" in sys.argv
+    ns = 1 if serial else 0  # n_splits for the split-KV launches
     dev = torch.device("cuda", 0)
     bf = torch.bfloat16
     # K1
@@ -53,29 +60,32 @@ def main():
     n = rows + 1
     # K2 decode (word-mode fold) and K2q query encode
     q1 = ops.prng_fill((1, 1, hq, d), 8, 1, 1.0, bf, dev)
-    ops.phase2_partial(q1, kp, vp, table.view(1, -1), kv_len, n)
+    ops.phase2_partial(q1, kp, vp, table.view(1, -1), kv_len, n, n_splits=ns)
     q32 = ops.prng_fill((1, 32, hq, d), 9, 1, 1.0, bf, dev)
-    ops.phase2_partial(q32, kp, vp, table.view(1, -1), kv_len, n, own_tail=32)
-    ops.phase2_partial(q1.float(), kp.float(), vp.float(), table.view(1, -1), kv_len, n)
+    ops.phase2_partial(q32, kp, vp, table.view(1, -1), kv_len, n, own_tail=32, n_splits=ns)
+    ops.phase2_partial(q1.float(), kp.float(), vp.float(), table.view(1, -1), kv_len, n,
+                       n_splits=ns)
     # exchanges: one-kernel (1 rank) and push + K3x (2 ranks' boxes in this process)
     ex1 = D.local_peer_exchanges(1, hq, hkv, d, dev)[0]
-    ex1.exchange(q1, kp, vp, table.view(1, -1), kv_len, n)
+    ex1.exchange(q1, kp, vp, table.view(1, -1), kv_len, n, n_splits=ns)
     exs = D.local_peer_exchanges(2, hq, hkv, d, dev)
     for r in range(2):
-        exs[r].push_partial(q1, kp, vp, table.view(1, -1), kv_len, n)
+        exs[r].push_partial(q1, kp, vp, table.view(1, -1), kv_len, n, n_splits=ns)
     for r in range(2):
         exs[r].merge(1, 1, hq, hkv)
-    o, s = ops.phase2_partial(q1, kp, vp, table.view(1, -1), kv_len, n)
+    o, s = ops.phase2_partial(q1, kp, vp, table.view(1, -1), kv_len, n, n_splits=ns)
     ops.merge(torch.stack([o.view(hq, d)] * 3), torch.stack([s.view(hq)] * 3))
     # fused decode (RoPE + append inside K2), with the current-position cos/sin, the counter
     # advance, and the fused decode through the one-kernel exchange (1 rank)
     posn = torch.tensor([n], dtype=torch.int64, device=dev)
     rope = ops.DecodeRope(n, 8, d, 10000.0, 1, dev)
     rope.prime(posn)
-    ops.phase2_decode(qn, kn, kn, posn, kp, vp, table.view(1, -1), kv_len, n + 1, table=rope)
+    ops.phase2_decode(qn, kn, kn, posn, kp, vp, table.view(1, -1), kv_len, n + 1, table=rope,
+                      n_splits=ns)
     ops.phase2_decode(qn, None, None, posn, kp, vp, table.view(1, -1), kv_len, n + 1, table=rope,
-                      append=False)
-    ex1.decode_exchange(qn, kn, kn, posn, kp, vp, table.view(1, -1), kv_len, n + 1, 10000.0, rope)
+                      append=False, n_splits=ns)
+    ex1.decode_exchange(qn, kn, kn, posn, kp, vp, table.view(1, -1), kv_len, n + 1, 10000.0, rope,
+                        n_splits=ns)
     ops.decode_advance(kv_len, posn, rope=rope)
     torch.cuda.synchronize()
     print("sanitize cases done")
