@@ -367,11 +367,12 @@ __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>:
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_half[i]);
+        if (seq && prm.seq == 2 && lane == 0) mbar_arrive(&seq_done[i * 4 + wq]);  // mid-row turn
       };
       const float rs = diag ? exp_pack_regs<true, POLY, SUM, SPLIT>(sv, s_tm, lim, sl2, m_use, half)
                             : exp_pack_regs<false, POLY, SUM, SPLIT>(sv, s_tm, lim, sl2, m_use, half);
       K1_TR(tr, (i * 256 + j) * 5 + 3);
-      if (seq) {
+      if (seq && prm.seq != 2) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&seq_done[i * 4 + wq]);
       }
