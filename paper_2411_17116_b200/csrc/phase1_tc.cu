@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>:
 }
 
 // ------------------------------------------------------------------ host
-constexpr int kDefaultSeq = 1;
+constexpr int kDefaultSeq = 0;  // MUFU ping-pong off: with a quarter of the exps on the FMA pipe it costs more than it saves
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;

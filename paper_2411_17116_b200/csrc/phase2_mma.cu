@@ -1110,7 +1110,12 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
                          (j > 0 || h > 0 || kk > 0) ? 1u : 0u);
         }
         K2Q_TR(true, j, 6);
-        if (j + 1 < ntiles) umma_commit_warp(&o_done[j % kSBuf]);  // waited by a rescale of j+1
+        if (j + 1 < ntiles) {  // waited by a rescale of tile j+1
+          // observe the barrier's previous phase (P.V(j - kSBuf), long complete) before arming
+          // the next, so every phase is waited once (compute-sanitizer synccheck)
+          if (j >= kSBuf) mbar_wait(&o_done[j % kSBuf], ((j / kSBuf) - 1) & 1);
+          umma_commit_warp(&o_done[j % kSBuf]);
+        }
         if (j == ntiles - 1) umma_commit_warp(o_last);
         if (j + VST < ntiles) umma_commit_warp(&v_empty[vs]);
         if (j + kSBuf < ntiles) issue_s(j + kSBuf);
