@@ -526,15 +526,16 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
   if (tiles == 0) return STAR_OK;
   // the product build instantiates the measured-best form: one-pass row in
   // registers, split P hand-off, fp32 FADD2 row sums, every 4th exponential pair on the FMA
-  // pipe, MUFU ping-pong of the two heads; NQ == 2 runs the 12-warp layout (setmaxnreg gives
-  // the softmax warpgroups 200 registers) with the MMA warp waiting without a suspend hint
+  // pipe; NQ == 2 runs the 12-warp layout (setmaxnreg gives the softmax warpgroups 200
+  // registers) with the MMA warp waiting without a suspend hint and issuing each MMA batch
+  // under one elect
   prm.seq = kDefaultSeq;
   if (const char* sq = getenv("STAR_K1_SEQ")) prm.seq = atoi(sq);  // measurement knob
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const P1Params);
   KernT kern;
   int threads;
   if constexpr (NQ == 2) {
-    kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0>;
+    kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0, true>;
     threads = C::kThreads12;
   } else {
     kern = phase1_tc_kernel<D, NQ, 4, 2, true, false, 1, false, 0>;
@@ -548,7 +549,7 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
     }
     if constexpr (NQ == 2) {
       if (vv == 2) kern = phase1_tc_kernel<D, NQ, 0, 2, true, true, 1, false, 0>;
-      if (vv == 3) kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0, true>;
+      if (vv == 3) kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0>;  // per-MMA elect
       if (vv == 4) kern = phase1_tc_kernel<D, NQ, 3, 2, true, true, 1, false, 0>;
       if (vv == 5) kern = phase1_tc_kernel<D, NQ, 2, 2, true, true, 1, false, 0>;
     }
