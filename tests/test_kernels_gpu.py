@@ -146,6 +146,30 @@ def test_phase1_tensor_core_bf16(ops, d, hq, hkv, seg_lens):
         np.testing.assert_allclose(t2n(lse), ref_lse, atol=BF16_TOL, rtol=0)
 
 
+@pytest.mark.parametrize("knob,value", [("STAR_K1_SM", "1"), ("STAR_K1_SM", "2"),
+                                        ("STAR_K1_SM", "3"), ("STAR_K1_SM", "4"),
+                                        ("STAR_K1_SM", "5"), ("STAR_K1_SEQ", "1"),
+                                        ("STAR_K1_SEQ", "2")])
+@pytest.mark.parametrize("d,hq,hkv,seg_lens", [(128, 8, 2, [128 * 3 + 17, 256]),
+                                               (64, 4, 2, [200, 384, 1])])
+def test_phase1_measurement_knobs(ops, monkeypatch, knob, value, d, hq, hkv, seg_lens):
+    """Every K1 form the measurement knobs select (the round-1 kernel, no FMA exp2,
+    per-MMA elect, other exp2 shares, the MUFU ping-pong) is checked against the fp64 oracle
+    like the default form."""
+    monkeypatch.setenv(knob, value)  # read by the launcher at every call
+    q, k, v, starts = _segments_inputs(seg_lens, hq, hkv, d, torch.bfloat16, seed=d + hq + 7)
+    ref, ref_lse = _oracle_segments(q, k, v, starts, hq, hkv)
+    out, lse = ops.phase1_fwd(q.cuda(), k.cuda(), v.cuda(), starts, want_lse=True,
+                              out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    got = t2n(out)
+    for h in range(hq):
+        for a, b in zip(starts[:-1], starts[1:]):
+            err = normwise(got[a:b, h], ref[a:b, h])
+            assert err <= BF16_TOL, (knob, value, h, a, b, err)
+    np.testing.assert_allclose(t2n(lse), ref_lse, atol=BF16_TOL, rtol=0)
+
+
 @pytest.mark.parametrize("d,hq,hkv,seg_lens", [(64, 4, 4, [100, 64, 33]), (16, 2, 1, [40, 7])])
 def test_phase1_fp32_check_mode(ops, d, hq, hkv, seg_lens):
     q, k, v, starts = _segments_inputs(seg_lens, hq, hkv, d, torch.float32, seed=5)
