@@ -319,7 +319,14 @@ __device__ void split_merge_words(int b, int kvh, int r_lo, int r_n, int lq, int
         }
         if (all) break;
         if (t0 == 0) t0 = globaltimer_ns();
-        if (globaltimer_ns() - t0 > pp.timeout_ns) __trap();  // a split never landed
+        if (globaltimer_ns() - t0 > pp.timeout_ns) {  // a split never landed: fail loudly
+          if ((threadIdx.x & 31) == 0)
+            printf("star K2 split fold timed out: block (%d,%d,%d) row %d col %d epoch %u "
+                   "splits %d-%d: lse word epoch %u\n", (int)blockIdx.x, (int)blockIdx.y,
+                   (int)blockIdx.z, rr, c, es, p0, p0 + PS - 1,
+                   (p0 < nsp) ? ld_word(w_lse + p0 * part_rows + orow).y : 0u);
+          __trap();
+        }
       }
       K2_TR(e == lo && p0 == 0, 4);
       float mn = m;
@@ -536,7 +543,12 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   const uint32_t ep = (gridDim.x == 1 && pp.L.world > 0) ? exchange_epoch(pp) : 0u;
   // word-mode split fix-up: this split's partial goes out as {value, epoch} words
   const bool words = grp_epoch != nullptr && gridDim.x > 1;
-  const uint32_t es = words ? next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y)) : 0u;
+  // read once per CTA (thread 0) before any word is stored, as K2q (see there)
+  __shared__ uint32_t es_sh;
+  if (threadIdx.x == 0)
+    es_sh = words ? next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y)) : 0u;
+  named_barrier_sync(1, NC * 32);
+  const uint32_t es = es_sh;
   uint2* const w_out = reinterpret_cast<uint2*>(out);
   uint2* const w_lse = w_out + (int64_t)gridDim.x * part_stride_rows * D;
   uint2* const wsp_out = w_out + (int64_t)split * part_stride_rows * D;
@@ -854,6 +866,13 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
 // P, as K2's mma.sync path, which keeps the 2e-3 parity bound (bf16 P alone measured 2.04e-3
 // at 5K keys).  Softmax as K1 (one thread per row = TMEM lane, lazy O rescale); padding rows
 // past G*l_q and keys past the split end or the row's own-tail limit are masked.
+// K2q's mbarrier waits: bounded and reporting (block, thread, site, parity) in a debug build
+// (-DSTAR_K2Q_DEBUG, `make debug`), plain otherwise
+#ifdef STAR_K2Q_DEBUG
+#define K2Q_WAIT(tag, bar, par) mbar_wait_dbg(bar, par, 100 + (tag))
+#else
+#define K2Q_WAIT(tag, bar, par) mbar_wait(bar, par)
+#endif
 namespace p2q {
 constexpr int BN = 128;                 // keys per tile
 constexpr int kSlab = 128 * 128;        // [128 rows x 64 bf16] SW128 slab
@@ -873,6 +892,10 @@ constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
 // warp 8 TMA, warp 9 MMA + TMEM allocation
 constexpr int kSoftmaxThreads = 256;
 constexpr int kThreads = kSoftmaxThreads + 64;
+// 12-warp form: + two idle warps, so warpgroup 2 (TMA, MMA) can hand registers to the softmax
+constexpr int kThreads12 = 384;
+constexpr int kRegsCtl = 88, kRegsSoftmax = 208;
+static_assert(4 * (168 - kRegsCtl) >= 8 * (kRegsSoftmax - 168), "register pool");
 constexpr int kSBuf = 3;                // S buffers in TMEM (3 x 128 + O 128 = 512 columns)
 constexpr int kOCol = kSBuf * BN;       // O after the S buffers
 static_assert(kSmem <= 232448, "shared memory budget");
@@ -944,8 +967,8 @@ __device__ __forceinline__ float exp_pack_hilo_half(const uint32_t (&sv)[2][32],
   return (rsum[0].x + rsum[0].y) + (rsum[1].x + rsum[1].y);
 }
 
-template <bool FS>
-__global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
+template <bool FS, bool L12 = false>
+__global__ void __launch_bounds__(L12 ? p2q::kThreads12 : p2q::kThreads, 1) phase2_qe_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
     const __grid_constant__ CUtensorMap tm_v, int lq, int hq, int hkv,
     const int32_t* __restrict__ page_table, int pages_per_seq, int page_size,
@@ -979,7 +1002,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
   uint2* const w_lse = w_out + (int64_t)gridDim.x * part_rows * D;
 
   // the Q tile's rows past G*l_q are never loaded: zero them (no garbage in their S rows)
-  for (int e = threadIdx.x; e < kTile / 16; e += kThreads)
+  for (int e = threadIdx.x; e < kTile / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(smem + kQOff)[e] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
@@ -998,6 +1021,16 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
   const uint32_t tbase = *tmem_slot;
   // programmatic dependent launch: the setup above overlapped the previous kernel
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the word-mode epoch of this launch, read ONCE per CTA before any of its words is stored:
+  // a CTA advances the group's epoch only after seeing every split's words, so every CTA of
+  // the group has read it by then — a later re-read could see the advanced value (round 2:
+  // the epilogue and the fold each re-read it, and a slow CTA folded against epoch + 1)
+  __shared__ uint32_t es_cta_sh;
+  if (threadIdx.x == 0)
+    es_cta_sh = (grp_epoch != nullptr && gridDim.x > 1)
+                    ? next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y)) : 0u;
+  __syncthreads();
+  const uint32_t es_cta = es_cta_sh;
   const int64_t len = kv_len[b];
   const int64_t r1 = min(len, r0 + chunk);
   const int64_t tail0 = len - own_tail;
@@ -1012,7 +1045,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     return (int)(((int64_t)page * hkv + kvh) * page_size + row % page_size);
   };
 
-  if (warp == 8) {
+  auto producer_role = [&]() {
     if (ntiles > 0) {
       // ================= TMA producer: Q once, then K (one tile ahead) and V =================
       // The whole warp resolves page-table entries 32 half-tiles at a time (lane l -> half
@@ -1045,7 +1078,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         if (lane == 0) {
           if (doK) {
             const int st = kt % KST;
-            if (kt >= KST) mbar_wait(&k_empty[st], ((kt / KST) + 1) & 1);
+            if (kt >= KST) K2Q_WAIT(1, &k_empty[st], ((kt / KST) + 1) & 1);
             mbar_expect_tx(&k_full[st], kTile);
             unsigned char* dst = smem + kKOff + st * kTile;
             for (int a = 0; a < 2; ++a) {
@@ -1054,7 +1087,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
             }
           } else {
             const int st = vt % VST;
-            if (vt >= VST) mbar_wait(&v_empty[st], ((vt / VST) + 1) & 1);
+            if (vt >= VST) K2Q_WAIT(2, &v_empty[st], ((vt / VST) + 1) & 1);
             mbar_expect_tx(&v_full[st], kTile);
             unsigned char* dst = smem + kVOff + st * kTile;
             for (int a = 0; a < 2; ++a) {
@@ -1067,7 +1100,8 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         if (doK) ++kt; else ++vt;
       }
     }
-  } else if (warp == 9) {
+  };
+  auto mma_role = [&]() {
     // ================= MMA issuer =================
     // S(j) -> buffer j%2.  Order: S(0), S(1), then per tile j: P.V(j) (hi + lo halves of the
     // buffer), S(j+2) into the same buffer (in-order execution: P(j) is consumed first).
@@ -1079,7 +1113,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       const uint32_t v_addr = smem_u32(smem + kVOff);
       auto issue_s = [&](int t) {
         const int st = t % KST;
-        mbar_wait(&k_full[st], (t / KST) & 1);
+        K2Q_WAIT(3, &k_full[st], (t / KST) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -1092,12 +1126,12 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         // release a stage only if the producer will refill it (commit only what is waited)
         if (t + KST < ntiles) umma_commit_warp(&k_empty[st]);
       };
-      mbar_wait(q_full, 0);
+      K2Q_WAIT(4, q_full, 0);
       for (int t = 0; t < kSBuf && t < ntiles; ++t) issue_s(t);
       for (int j = 0; j < ntiles; ++j) {
         const int vs = j % VST;
-        mbar_wait(&v_full[vs], (j / VST) & 1);
-        mbar_wait(&p_full[j % kSBuf], (j / kSBuf) & 1);
+        K2Q_WAIT(5, &v_full[vs], (j / VST) & 1);
+        K2Q_WAIT(6, &p_full[j % kSBuf], (j / kSBuf) & 1);
         tc_fence_after();
         K2Q_TR(true, j, 5);
         const uint32_t pb = tbase + (j % kSBuf) * BN;
@@ -1113,7 +1147,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         if (j + 1 < ntiles) {  // waited by a rescale of tile j+1
           // observe the barrier's previous phase (P.V(j - kSBuf), long complete) before arming
           // the next, so every phase is waited once (compute-sanitizer synccheck)
-          if (j >= kSBuf) mbar_wait(&o_done[j % kSBuf], ((j / kSBuf) - 1) & 1);
+          if (j >= kSBuf) K2Q_WAIT(7, &o_done[j % kSBuf], ((j / kSBuf) - 1) & 1);
           umma_commit_warp(&o_done[j % kSBuf]);
         }
         if (j == ntiles - 1) umma_commit_warp(o_last);
@@ -1125,10 +1159,11 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
       // the running max jumps): no commit arrival is left unobserved when the CTA exits
       for (int i = 0; i < kSBuf; ++i) {
         const int n_i = ntiles - 1 > i ? (ntiles - 1 - i + kSBuf - 1) / kSBuf : 0;
-        if (n_i > 0) mbar_wait(&o_done[i], (n_i - 1) & 1);
+        if (n_i > 0) K2Q_WAIT(8, &o_done[i], (n_i - 1) & 1);
       }
     }
-  } else {
+  };
+  auto softmax_role = [&]() {
     // ================= softmax: warps w and w+4 share the rows of TMEM lane quarter w%4,
     // each on one 64-column half of every S row (two warps per SM sub-partition keep its
     // MUFU pipe busy); the halves swap their row maxima through shared memory =================
@@ -1149,7 +1184,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     const int last_rel = pad ? INT_MAX / 2 : (int)(min(r1 - 1, tail0 + ti) - r0);
     for (int j = 0; j < ntiles; ++j) {
       const uint32_t s_tm = tbase + lane_off + (j % kSBuf) * BN;
-      mbar_wait(&s_full[j % kSBuf], (j / kSBuf) & 1);
+      K2Q_WAIT(9, &s_full[j % kSBuf], (j / kSBuf) & 1);
       tc_fence_after();
       K2Q_TR(threadIdx.x == 0, j, 0);
       const int64_t base = r0 + (int64_t)j * BN;
@@ -1186,7 +1221,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         // keys past the split end: their V rows may hold stale (even non-finite) data and
         // P = 0 must not meet a NaN — zero them (half h clears V slab h) once the tile landed
         const int valid = (int)(r1 - base);
-        mbar_wait(&v_full[j % VST], (j / VST) & 1);
+        K2Q_WAIT(10, &v_full[j % VST], (j / VST) & 1);
         if (r >= valid) {
           uint4* vrow = reinterpret_cast<uint4*>(smem + kVOff + (j % VST) * kTile + hf * kSlab + r * 128);
 #pragma unroll
@@ -1199,7 +1234,7 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         // completes once per kSBuf tiles: P.V(j-1-kSBuf) is done (S(j) was issued after
         // P.V(j-kSBuf)) and P.V(j-1+kSBuf) cannot be (it needs a later P), so the parity of
         // ((j-1) / kSBuf) is unambiguous
-        mbar_wait(&o_done[(j - 1) % kSBuf], ((j - 1) / kSBuf) & 1);
+        K2Q_WAIT(11, &o_done[(j - 1) % kSBuf], ((j - 1) / kSBuf) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -1225,11 +1260,11 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
     named_barrier_sync(2, kSoftmaxThreads);
     const float l_row = l_run + lsum[(hf ^ 1) * 128 + r];
     const bool single = gridDim.x == 1;
-    const uint32_t es = single ? 0u : next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y));
+    const uint32_t es = single ? 0u : es_cta;
     const uint32_t ep = (single && pp.L.world > 0) ? exchange_epoch(pp) : 0u;
     if (ntiles > 0) {
       // (not o_done's parity: P.V(ntiles-2) may still be in flight here, two phases behind)
-      mbar_wait(o_last, 0);
+      K2Q_WAIT(12, o_last, 0);
       tc_fence_after();
     }
     const bool row_ok = r < QR;
@@ -1266,15 +1301,37 @@ __global__ void __launch_bounds__(p2q::kThreads, 1) phase2_qe_kernel(
         st_word(w_lse + (int64_t)split * part_rows + orow, lv, es);
     }
     tc_fence_before();
+    if (gridDim.x > 1) {
+      // word-mode fold of the splits (+ the peer exchange push / merge when asked); it reads
+      // only global words, so it runs before the CTA-wide barrier that precedes the TMEM free
+      split_merge_words<D, kSoftmaxThreads>(b, kvh, 0, QR, lq, hq, G, w_out, w_lse, part_rows, es_cta,
+                                            final_out, final_lse, grp_epoch, pp);
+    }
+  };
+  if (L12) {
+    // 12 warps: warpgroup 2 (TMA, MMA, two idle warps) gives registers to the softmax
+    // warpgroups (setmaxnreg inside warpgroup-uniform branches, as K1)
+    const int wg = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 7), 0);
+    if (wg == 2) {
+      regs_dealloc<kRegsCtl>();
+      if (warp == 8)
+        producer_role();
+      else if (warp == 9)
+        mma_role();
+    } else {
+      regs_alloc<kRegsSoftmax>();
+      softmax_role();
+    }
+  } else {
+    if (warp == 8)
+      producer_role();
+    else if (warp == 9)
+      mma_role();
+    else
+      softmax_role();
   }
   __syncthreads();
   if (warp == 9) tmem_free<512>(tbase);
-  if (warp < 8 && gridDim.x > 1) {
-    // word-mode fold of the splits (+ the peer exchange push / merge when asked)
-    const uint32_t es = next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y));
-    split_merge_words<D, kSoftmaxThreads>(b, kvh, 0, QR, lq, hq, G, w_out, w_lse, part_rows, es,
-                                          final_out, final_lse, grp_epoch, pp);
-  }
 }
 
 // ------------------------------------------------------------------ host
@@ -1372,6 +1429,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
   // the in-kernel cross-rank merge needs the co-resident word-mode grid
   if (pp.merge && (grp_epoch == nullptr || pp.L.world == 0)) pp.merge = 0;
   if (merged != nullptr) *merged = pp.merge;
+  bool reset_now = false;
   if (n_splits > 1 && counters != nullptr) {
     // A word's slot position depends on (batch, lq, hq, hkv, d) and word-mode epochs count
     // per (sequence, kv head): a workspace reused with another shape (or after the
@@ -1390,6 +1448,10 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
       cudaError_t e = cudaMemsetAsync(counters, 0, bytes, s);
       if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 workspace reset: %s", cudaGetErrorString(e));
       last[counters] = sig;
+      // a programmatic-dependent launch is not ordered after this memset (measured: with the
+      // workspace address reused by another shape, the zeroing landed while the kernel's words
+      // were in flight and the fold never completed) — this launch goes without PDL
+      reset_now = true;
     }
   }
   if (use_qe) {
@@ -1409,7 +1471,13 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
       const char* ev = getenv("STAR_K2Q_SUM");
       fs = (ev != nullptr && ev[0] == '0') ? 0 : 1;
     }
-    auto qek = fs ? phase2_qe_kernel<true> : phase2_qe_kernel<false>;
+    static int l12 = -1;  // STAR_K2Q_L12=0: the 10-warp form (measurement knob)
+    if (l12 < 0) {
+      const char* ev = getenv("STAR_K2Q_L12");
+      l12 = (ev != nullptr && ev[0] == '0') ? 0 : 1;
+    }
+    auto qek = fs ? (l12 ? phase2_qe_kernel<true, true> : phase2_qe_kernel<true, false>)
+                  : (l12 ? phase2_qe_kernel<false, true> : phase2_qe_kernel<false, false>);
     cudaError_t e = cudaFuncSetAttribute(qek,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, p2q::kSmem);
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 qe smem attr: %s", cudaGetErrorString(e));
@@ -1419,13 +1487,13 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
       attr[na].id = cudaLaunchAttributeCooperative;
       attr[na++].val.cooperative = 1;
     }
-    if (k2_pdl()) {
+    if (k2_pdl() && !reset_now) {
       attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[na++].val.programmaticStreamSerializationAllowed = 1;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(p2q::kThreads);
+    cfg.blockDim = dim3(l12 ? p2q::kThreads12 : p2q::kThreads);
     cfg.dynamicSmemBytes = p2q::kSmem;
     cfg.stream = s;
     cfg.attrs = attr;
@@ -1452,7 +1520,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
       attr[na].id = cudaLaunchAttributeCooperative;                                             \
       attr[na++].val.cooperative = 1;                                                           \
     }                                                                                           \
-    if (k2_pdl()) {                                                                             \
+    if (k2_pdl() && !reset_now) {                                                                             \
       attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;                         \
       attr[na++].val.programmaticStreamSerializationAllowed = 1;                                \
     }                                                                                           \
