@@ -90,9 +90,13 @@ __device__ __forceinline__ uint32_t swz(uint32_t slab, int row, int chunk) {
 // K2 timeline (tracing library only, tools/k2_trace.py): per CTA, globaltimer ns at
 // [0] entry, [1] first K/V tile landed (consumer warp 0), [2] main loop done (warp 0),
 // [3] split partial stored (thread 0), [4] fix-up: all splits' words seen, [5] exit
-// (thread 0), [6] fused exchange: every rank's words seen, [7] fused exchange: arrived.
+// (thread 0), [6] fused exchange: every rank's words seen, [7] fused exchange: arrived,
+// [8] kv_len loaded after griddepcontrol.wait (thread 0), [9] main loop done (warp 4, the
+// other tile group), [10] every warp's loop done (decode merge, first barrier), [11] warp
+// partials staged (second barrier).
+constexpr int kK2TrSlots = 12;
 constexpr int kK2TrCtas = 2048;
-__device__ unsigned long long g_k2_trace[kK2TrCtas][8];
+__device__ unsigned long long g_k2_trace[kK2TrCtas][kK2TrSlots];
 __device__ __forceinline__ void k2_tr(int slot) {
   const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   if (cta < kK2TrCtas) {
@@ -446,8 +450,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   constexpr int NC = Cons<KEYSPLIT>::NC, NG = Cons<KEYSPLIT>::NG;
   constexpr int NT_D = D / 8;  // n-tiles over head dim (P.V output)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* smem = smem_align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kBarOff);
   uint64_t* empty = full + ST;
 
@@ -488,11 +491,12 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
   // append that writes q's row and bumps kv_len): everything above overlapped that kernel;
   // nothing it writes is read before this point.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int64_t base_len = kv_len[b];
+  const int64_t base_len = ld_after_wait(kv_len + b);
   const int64_t len = base_len + (ap.on ? ap.add : 0);
   const int64_t r1 = min(len, r0 + chunk);
   const int64_t tail0 = len - own_tail;
   const int ntiles = r1 > r0 ? (int)((r1 - r0 + TN - 1) / TN) : 0;
+  K2_TR(threadIdx.x == 0 && ntiles >= 0, 8);
 
   if (warp == NC) {
     // ================= TMA producer =================
@@ -754,6 +758,7 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
       if (lane == 0) mbar_arrive(&empty[st]);
     }
     K2_TR(threadIdx.x == 0, 2);
+    K2_TR(threadIdx.x == 128, 9);
     // row sums across the quad
     lA += __shfl_xor_sync(0xffffffffu, lA, 1);
     lA += __shfl_xor_sync(0xffffffffu, lA, 2);
@@ -768,7 +773,10 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
       float* so = reinterpret_cast<float*>(smem);             // [NC][16][SR]
       float* sm = so + NC * 16 * SR;                          // [NC][16] max
       float* sl = sm + NC * 16;                               // [NC][16] sum
+      float* sw = sl + NC * 16;                               // [NC][16] merge weight
+      float* slse = sw + NC * 16;                             // [16] row lse
       named_barrier_sync(1, NC * 32);
+      K2_TR(threadIdx.x == 0, 10);
 #pragma unroll
       for (int n = 0; n < NT_D; ++n) {
         const int c = n * 8 + t4 * 2;
@@ -785,30 +793,45 @@ __global__ void __launch_bounds__(p2::Cons<KEYSPLIT>::kThreads) phase2_mma_kerne
         sl[warp * 16 + g4 + 8] = lB;
       }
       named_barrier_sync(1, NC * 32);
-      for (int e = threadIdx.x; e < QR * D; e += NC * 32) {
-        const int rr = e / D, c = e % D;
+      // one thread per row: the warp weights 2^(m_w - m) / l of the row (so the element pass
+      // below is a weighted sum with no exponential, division or logarithm) and its lse
+      if (threadIdx.x < QR) {
+        const int rr = threadIdx.x;
         float m = -INFINITY;
 #pragma unroll
         for (int w = 0; w < NC; ++w) m = fmaxf(m, sm[w * 16 + rr]);
-        float l = 0.f, acc = 0.f;
-        if (m > -INFINITY) {
+        float f[NC], l = 0.f;
 #pragma unroll
-          for (int w = 0; w < NC; ++w) {
-            const float f = ex2(sm[w * 16 + rr] - m);
-            l += sl[w * 16 + rr] * f;
-            acc += so[(w * 16 + rr) * SR + c] * f;
-          }
+        for (int w = 0; w < NC; ++w) {
+          f[w] = m > -INFINITY ? ex2(sm[w * 16 + rr] - m) : 0.f;
+          l += sl[w * 16 + rr] * f[w];
+        }
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int w = 0; w < NC; ++w) sw[w * 16 + rr] = f[w] * inv;
+        slse[rr] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+      }
+      named_barrier_sync(1, NC * 32);
+      K2_TR(threadIdx.x == 0, 11);
+      // two adjacent columns per thread (one 16-byte word pair / float2 store)
+      for (int e = threadIdx.x; e < QR * (D / 2); e += NC * 32) {
+        const int rr = e / (D / 2), c = 2 * (e % (D / 2));
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < NC; ++w) {
+          const float2 ov = *reinterpret_cast<const float2*>(so + (w * 16 + rr) * SR + c);
+          const float wt = sw[w * 16 + rr];
+          acc.x = fmaf(ov.x, wt, acc.x);
+          acc.y = fmaf(ov.y, wt, acc.y);
         }
         const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
         // one split: this is the final partial (pushed to every rank's box when exchanging)
-        const float vo = l > 0.f ? acc / l : 0.f;
-        const float vl = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
         if (words) {
-          st_word(wsp_out + orow * D + c, vo, es);
-          if (c == 0) st_word(wsp_lse + orow, vl, es);
+          st_word2(wsp_out + orow * D + c, acc, es);
+          if (c == 0) st_word(wsp_lse + orow, slse[rr], es);
         } else {
-          put_out(pp, ep, gridDim.x > 1, out_part, orow * D + c, vo);
-          if (c == 0) put_lse(pp, ep, gridDim.x > 1, lse_part, orow, vl);
+          put_out2(pp, ep, gridDim.x > 1, out_part, orow * D + c, acc);
+          if (c == 0) put_lse(pp, ep, gridDim.x > 1, lse_part, orow, slse[rr]);
         }
       }
     } else {
@@ -978,6 +1001,8 @@ __global__ void __launch_bounds__(L12 ? p2q::kThreads12 : p2q::kThreads, 1) phas
   using namespace p2q;
   constexpr int D = 128;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // the generic-pointer derivation is kept here: with smem_align1024 (LDS/STS for the
+  // epilogue's staging) K2q measured 1.5% slower (query encode at 128K, l_q = 8 and 32)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
@@ -1031,7 +1056,7 @@ __global__ void __launch_bounds__(L12 ? p2q::kThreads12 : p2q::kThreads, 1) phas
                     ? next_epoch(__ldcg(grp_epoch + b * gridDim.y + blockIdx.y)) : 0u;
   __syncthreads();
   const uint32_t es_cta = es_cta_sh;
-  const int64_t len = kv_len[b];
+  const int64_t len = ld_after_wait(kv_len + b);
   const int64_t r1 = min(len, r0 + chunk);
   const int64_t tail0 = len - own_tail;
   const int ntiles = r1 > r0 ? (int)((r1 - r0 + BN - 1) / BN) : 0;
@@ -1349,6 +1374,17 @@ static bool k2_pdl() {
   return on == 1;
 }
 
+// STAR_K2_COOP=0 launches the word-mode grid without the cooperative attribute (measurement
+// only: co-residency then rests on an otherwise idle GPU)
+static bool k2_coop() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("STAR_K2_COOP");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // K2q (tcgen05 query encode) takes 16 < G*l_q <= 128 packed rows at head_dim 128 over a pool
 // of 64-key-aligned pages; STAR_K2_QE=0 turns it off (measurement)
 bool phase2_qe_eligible(int qrows, int d, int page_size) {
@@ -1483,7 +1519,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 qe smem attr: %s", cudaGetErrorString(e));
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (grp_epoch != nullptr) {  // cooperative only for the word-mode fold
+    if (grp_epoch != nullptr && k2_coop()) {  // cooperative only for the word-mode fold
       attr[na].id = cudaLaunchAttributeCooperative;
       attr[na++].val.cooperative = 1;
     }
@@ -1516,7 +1552,7 @@ int phase2_mma(const void* q, int batch, int lq, int hq, int hkv, int d, const v
     if (e != cudaSuccess) return fail(STAR_ECUDA, "phase2 smem attr: %s", cudaGetErrorString(e)); \
     cudaLaunchAttribute attr[2];                                                                \
     int na = 0;                                                                                 \
-    if (grp_epoch != nullptr) {                                                                 \
+    if (grp_epoch != nullptr && k2_coop()) {                                                    \
       attr[na].id = cudaLaunchAttributeCooperative;                                             \
       attr[na++].val.cooperative = 1;                                                           \
     }                                                                                           \
@@ -1557,7 +1593,7 @@ int debug_k2q_trace(long long* host, int n) {
   return cudaMemcpyFromSymbol(host, g_k2q_trace, n * sizeof(long long)) == cudaSuccess ? n : -4;
 }
 int debug_k2_trace(unsigned long long* host, int n) {
-  const int cap = kK2TrCtas * 8;
+  const int cap = kK2TrCtas * kK2TrSlots;
   if (n > cap) n = cap;
   return cudaMemcpyFromSymbol(host, g_k2_trace, n * sizeof(unsigned long long)) == cudaSuccess ? n : -4;
 }

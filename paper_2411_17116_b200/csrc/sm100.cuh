@@ -12,6 +12,20 @@ namespace sm100 {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// A global load that stays after griddepcontrol.wait: a load through a const __restrict__
+// pointer compiles to ld.global.nc, which the compiler may hoist above the wait (and did, for
+// K2's kv_len) — reading the counter before the previous kernel's store of it is visible.
+__device__ __forceinline__ int32_t ld_after_wait(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// The 1024-byte aligned base of dynamic shared memory, as an offset from the shared array
+// itself: the compiler keeps the shared address space (LDS/STS), where a round trip through
+// uintptr_t turns every access through the pointer into a generic LD/ST.
+__device__ __forceinline__ unsigned char* smem_align1024(unsigned char* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
 
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

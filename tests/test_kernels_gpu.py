@@ -533,6 +533,62 @@ def test_phase2_decode_equals_append_then_k2(ops, B, hq, hkv, d, starts, use_tab
     assert torch.equal(o2, o3) and torch.equal(l2, l3)
 
 
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("n_splits", [0, 1])
+def test_decode_chain_reads_the_current_counter(ops, fused, n_splits):
+    """K2 is launched as a programmatic dependent (PDL) of the kernel before it, and the one
+    before it may have just written the row counter: star_kv_append triggers its dependents at
+    entry and bumps kv_len at its end; star_decode_advance bumps every counter.  K2 must read
+    kv_len after griddepcontrol.wait — through a const __restrict__ pointer the compiler had
+    hoisted the load above it.  T chained steps on one stream with a primed workspace (so
+    every K2 launch is PDL), each step's (out, lse) equal, bit for bit, to K2 rerun on that
+    step's state after a device sync.  n_splits = 1 is a plain (not cooperative) launch, the
+    one that overlaps its predecessor the most."""
+    B, hq, hkv, d, page, T = 1, 32, 8, 128, 128, 24
+    start = 3000
+    maxk = start + T + 64
+    pps = -(-maxk // page)
+    dev = torch.device("cuda")
+    torch.manual_seed(5)
+    q = torch.randn(B, hq, d).bfloat16().cuda()
+    k = torch.randn(B, hkv, d).bfloat16().cuda()
+    v = torch.randn(B, hkv, d).bfloat16().cuda()
+    table = torch.arange(pps, dtype=torch.int32, device=dev).view(B, pps)
+    kp = ops.prng_fill((pps, hkv, page, d), 3, 1, 1.0, torch.bfloat16, dev)
+    vp = ops.prng_fill((pps, hkv, page, d), 4, 1, 1.0, torch.bfloat16, dev)
+    pos = torch.tensor([start + 11], dtype=torch.int64, device=dev)
+    kl = torch.tensor([start], dtype=torch.int32, device=dev)
+    rope = ops.DecodeRope(start + 11, T + 8, d, 10000.0, B, dev) if fused else None
+    ws = ops.Phase2Workspace()
+    ns = n_splits
+    ops.phase2_partial(q.view(B, 1, hq, d), kp, vp, table, kl, maxk, n_splits=ns, workspace=ws)  # prime
+    if fused:
+        rope.prime(pos)
+    steps = []
+    for _ in range(T):
+        if fused:
+            o, l = ops.phase2_decode(q, k, v, pos, kp, vp, table, kl, maxk, table=rope,
+                                     n_splits=ns, workspace=ws)
+            ops.decode_advance(kl, pos, rope=rope)
+            steps.append((None, o, l))
+        else:
+            qr = ops.kv_append(q, k, v, pos, kl, kp, vp, table)
+            o, l = ops.phase2_partial(qr.view(B, 1, hq, d), kp, vp, table, kl, maxk, n_splits=ns,
+                                      workspace=ws)
+            pos.add_(1)
+            steps.append((qr, o, l))
+    torch.cuda.synchronize()
+    assert int(kl[0]) == start + T
+    for t, (qr, o, l) in enumerate(steps):
+        kl_t = torch.tensor([start + t + 1], dtype=torch.int32, device=dev)
+        if qr is None:  # the fused step attended over its own new row: rerun unfused on it
+            qr = ops.rope(q, torch.tensor([start + 11 + t], dtype=torch.int64, device=dev))
+        o2, l2 = ops.phase2_partial(qr.view(B, 1, hq, d), kp, vp, table, kl_t, maxk, n_splits=ns,
+                                    workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(o, o2) and torch.equal(l, l2), t
+
+
 def test_phase2_decode_exchange_equals_unfused(ops):
     """The fused decode step through the one-kernel peer exchange (2 ranks' boxes on one GPU,
     one stream per rank, grids small enough to be co-resident as on separate GPUs) equals the

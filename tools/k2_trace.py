@@ -57,17 +57,20 @@ for _ in range(20):
     else:
         ops.phase2_partial(q, kp, vp, table, kv_len, a.rows, n_splits=splits, workspace=ws)
 torch.cuda.synchronize()
-N = 2048 * 8
+S = 12  # slots per CTA (phase2_mma.cu kK2TrSlots)
+N = 2048 * S
 buf = (ctypes.c_ulonglong * N)()
 lib.star_debug_k2_trace.restype = ctypes.c_int
 lib.star_debug_k2_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 lib.star_debug_k2_trace(buf, N)
-t = np.frombuffer(buf, dtype=np.uint64).reshape(2048, 8)[:ncta].astype(np.int64)
+t = np.frombuffer(buf, dtype=np.uint64).reshape(2048, S)[:ncta].astype(np.int64)
 t0 = t[:, 0].min()
 names = ["entry", "first tile", "loop done", "stored", "fixup seen", "exit", "xchg seen",
-         "xchg arrived"]
+         "xchg arrived", "kv_len read", "loop done g1", "all loops", "staged"]
+order = [0, 8, 1, 2, 9, 10, 11, 3, 4, 5, 6, 7]
 print(f"rows={a.rows} batch={a.batch} splits={splits} ctas={ncta}")
-for j, nm in enumerate(names):
+for j in order:
+    nm = names[j]
     col = t[:, j]
     col = col[col > 0] - t0
     if len(col):
