@@ -12,6 +12,9 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("STAR_LIB_PATH"):  # A/B against another build
+    from paper_2411_17116_b200 import _lib  # noqa: E402
+    _lib.LIB_PATH = os.environ["STAR_LIB_PATH"]
 from paper_2411_17116_b200 import ops  # noqa: E402
 
 rows_list = [int(x) for x in sys.argv[1:]] or [256, 1024, 4096, 16384, 32768]
@@ -38,7 +41,7 @@ def graph_us(step):
     return e0.elapsed_time(e1) / T / L * 1e3
 
 
-env = {k: os.environ[k] for k in os.environ if k.startswith("STAR_K2")}
+env = {k: os.environ[k] for k in os.environ if k.startswith("STAR_K2") or k == "STAR_LIB_PATH"}
 res = {"env": env, "rows": rows_list, "k2": [], "decode": []}
 q = ops.prng_fill((1, hq, d), 90, 1, 1.0, torch.bfloat16, dev)
 kn = ops.prng_fill((1, hkv, d), 91, 1, 1.0, torch.bfloat16, dev)
