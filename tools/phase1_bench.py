@@ -7,6 +7,9 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("STAR_LIB_PATH"):  # A/B against another build
+    from paper_2411_17116_b200 import _lib  # noqa: E402
+    _lib.LIB_PATH = os.environ["STAR_LIB_PATH"]
 from paper_2411_17116_b200 import ops  # noqa: E402
 
 p = argparse.ArgumentParser()
