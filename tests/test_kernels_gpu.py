@@ -340,6 +340,50 @@ def test_sharp_scores_rescale_paths(ops, direction):
             np.testing.assert_allclose(t2n(l)[0, :, h], rl, atol=BF16_TOL, rtol=0)
 
 
+def test_known_answers_on_the_kernels(ops):
+    """SPEC's closed-form answers (tests/test_oracle.py checks them on the oracle) through the
+    product kernels: the 2 x 2 analytic causal attention on K1 — identity q, k,
+    v in the first two of 128 dimensions, so row 0 = v0 and row 1 = (v0 + e v1) / (1 + e) with
+    e = exp(1 / sqrt(d)) — and the ln 2 lse shift of a duplicated key set on K2
+    decode, K2q query encode and the fp32 check mode, output unchanged."""
+    d = 128
+    x = torch.zeros(2, 1, d)
+    x[0, 0, 0] = x[1, 0, 1] = 1.0
+    xb = x.bfloat16().cuda()
+    out, lse = ops.phase1_fwd(xb, xb, xb, [0, 2], want_lse=True, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    e = float(np.exp(1 / np.sqrt(d)))
+    ref = np.zeros((2, d))
+    ref[0, 0] = 1.0
+    ref[1, 0], ref[1, 1] = 1 / (1 + e), e / (1 + e)
+    np.testing.assert_allclose(t2n(out)[:, 0], ref, atol=BF16_TOL)
+    assert float(out[0, 0, 0]) == 1.0  # one visible key: P = 1 exactly
+    np.testing.assert_allclose(t2n(lse)[0], [1 / np.sqrt(d), np.log(1 + e)], atol=BF16_TOL)
+    # duplicated keys: the same cache twice -> lse + ln 2, same output
+    gen = torch.Generator().manual_seed(2)
+    n, hq, hkv, page = 1000, 8, 2, 64
+    for dtype, lq, tol in ((torch.bfloat16, 1, BF16_TOL), (torch.bfloat16, 32, BF16_TOL),
+                           (torch.float32, 1, 1e-5)):
+        k = torch.randn(n, hkv, d, generator=gen).to(dtype)
+        v = torch.randn(n, hkv, d, generator=gen).to(dtype)
+        q = torch.randn(1, lq, hq, d, generator=gen).to(dtype).cuda()
+        res = []
+        for reps in (1, 2):
+            rows = n * reps
+            pps = -(-rows // page)
+            kp = torch.zeros((pps, hkv, page, d), dtype=dtype, device="cuda")
+            vp = torch.zeros_like(kp)
+            table = torch.arange(pps, dtype=torch.int32, device="cuda").view(1, pps)
+            ops.kv_write(k.repeat(reps, 1, 1).cuda(), v.repeat(reps, 1, 1).cuda(), kp, vp,
+                         table[0].contiguous(), 0)
+            kv_len = torch.tensor([rows], dtype=torch.int32, device="cuda")
+            res.append(ops.phase2_partial(q, kp, vp, table, kv_len, rows))
+        torch.cuda.synchronize()
+        (o1, l1), (o2, l2) = res
+        assert normwise(t2n(o2), t2n(o1)) <= tol, (dtype, lq)
+        np.testing.assert_allclose(t2n(l2) - t2n(l1), np.log(2), atol=tol)
+
+
 def test_phase2_workspace_reuse_across_shapes(ops):
     """One workspace, alternating shapes and split counts (query encode -> decode -> batch):
     the word-mode fix-up's epochs and words must never pick up a stale word of another
