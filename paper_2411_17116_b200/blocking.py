@@ -232,6 +232,22 @@ class PagedKVPool:
         if rows > self.capacity:
             self._alloc(rows if exact else max(rows, 2 * self.capacity))
 
+    def head_view(self, layer: int, head: int):
+        """One kv head of `layer` as a single-head pool: (k, v, page_table), k/v viewed as
+        [num_pages * hkv, 1, page_size, d] (no copy) and the table remapped to
+        page * hkv + head, so K2 streams that head's rows only (one channel of
+        ss/sim.py:216-237 reads 1/hkv of the layer's bytes)."""
+        n_pages = self.k.shape[1]
+        shape = (n_pages * self.hkv, 1, self.page_size, self.head_dim)
+        key = (n_pages, head)
+        cache = getattr(self, "_head_tables", None)
+        if cache is None or cache[0] is not self.page_table:
+            cache = self._head_tables = (self.page_table, {})
+        table = cache[1].get(key)
+        if table is None:
+            table = cache[1][key] = (self.page_table * self.hkv + head).to(torch.int32)
+        return self.k[layer].view(shape), self.v[layer].view(shape), table
+
     @property
     def workspace(self):
         """This pool's K2 split workspace (one per pool, so the hosts' launches never share

@@ -255,13 +255,13 @@ def run_phase2_step(hosts: list[Host], q, own_tail: int = 0, ledger: CommLedger 
             if cache.rows == 0:
                 continue
             pool = cache.pool
-            qq = torch.zeros((1, qc.shape[0], pool.hkv, qc.shape[1]), dtype=pool.dtype,
-                             device=qc.device)
-            qq[0, :, cache.head] = qc.to(pool.dtype)
-            o, s = ops.phase2_partial(qq, pool.k[cache.layer], pool.v[cache.layer],
-                                      pool.page_table.view(1, -1), pool.kv_len_tensor(cache.layer),
-                                      cache.rows, own_tail=own_tail if host is qh else 0)
-            parts.append(PartialAttention(o[0, :, cache.head].to(qc.dtype), s[0, :, cache.head]))
+            # the channel's kv head as a one-head pool: K2 streams that head's rows only
+            kh, vh, table = pool.head_view(cache.layer, cache.head)
+            qq = qc.to(pool.dtype).reshape(1, qc.shape[0], 1, qc.shape[1]).contiguous()
+            o, s = ops.phase2_partial(qq, kh, vh, table.view(1, -1),
+                                      pool.kv_len_tensor(cache.layer), cache.rows,
+                                      own_tail=own_tail if host is qh else 0)
+            parts.append(PartialAttention(o[0, :, 0].to(qc.dtype), s[0, :, 0]))
             if host is not qh:
                 for kind, count in ((PARTIAL_OUT, qc.shape[0] * qc.shape[1]),
                                     (PARTIAL_LSE, qc.shape[0])):

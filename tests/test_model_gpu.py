@@ -120,6 +120,43 @@ def test_run_phase2_step_single_channel(S):
     assert [(e.src, e.dst, e.kind) for e in delta[:2]] == [(0, 3, "partial_out"), (0, 3, "partial_lse")]
 
 
+@pytest.mark.parametrize("dtype,d,lq", [("float32", 64, 3), ("bfloat16", 128, 1),
+                                        ("bfloat16", 128, 32)])
+def test_run_phase2_step_pool_channels(S, dtype, d, lq):
+    """Channels that are (layer, head) views of a multi-head host pool: each channel's K2
+    call streams its own kv head only (PagedKVPool.head_view); the merged output equals
+    attention over that head's rows of every host (ss/sim.py:216-237)."""
+    dt = getattr(torch, dtype)
+    rng = np.random.default_rng(5)
+    layers, hkv, n_hosts = 2, 4, 3
+    rows = [200, 64, 131]
+    hosts, dense = [], []
+    for i in range(n_hosts):
+        pool = S.PagedKVPool(layers, hkv, d, rows[i], page_size=64, dtype=dt, device="cuda")
+        kk = rng.uniform(-1, 1, (layers, rows[i], hkv, d)).astype(np.float32)
+        vv = rng.uniform(-1, 1, (layers, rows[i], hkv, d)).astype(np.float32)
+        for li in range(layers):
+            pool.append(li, torch.tensor(kk[li]).cuda(), torch.tensor(vv[li]).cuda(),
+                        range(rows[i]))
+        # the pool stores dt: the oracle sees the stored (rounded) values
+        dense.append((torch.tensor(kk).to(dt).float().numpy(), torch.tensor(vv).to(dt).float().numpy()))
+        hosts.append(S.Host(i, [S.KVCache(pool=pool, layer=li, head=h, host=i)
+                                for li in range(layers) for h in range(hkv)], pool=pool))
+    qs = [torch.tensor(rng.uniform(-1, 1, (lq, d)).astype(np.float32)).to(dt).cuda()
+          for _ in range(layers * hkv)]
+    outs, _ = S.run_phase2_step(hosts, qs)
+    # bf16: the kernel bound (2e-3) plus the rounding of the merged output to the query
+    # dtype (half an ulp, 2^-9 relative)
+    tol = 1e-5 if dtype == "float32" else 2e-3 + 2.0 ** -9
+    for c, (o, qc) in enumerate(zip(outs, qs)):
+        li, h = divmod(c, hkv)
+        ref, _ = O.partial_attention(qc.float().cpu().numpy().astype(np.float64),
+                                     np.concatenate([k[li, :, h] for k, _ in dense]).astype(np.float64),
+                                     np.concatenate([v[li, :, h] for _, v in dense]).astype(np.float64))
+        err = np.abs(o.float().cpu().numpy() - ref).max() / np.abs(ref).max()
+        assert err <= tol, (c, err)
+
+
 def test_drop_in_attention_functions(S, golden_dir):
     g = np.load(os.path.join(golden_dir, "attention.npz"))
     out = S.causal_attention(g["c1_q"], g["c1_k"], g["c1_v"])
