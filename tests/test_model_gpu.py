@@ -120,12 +120,15 @@ def test_run_phase2_step_single_channel(S):
     assert [(e.src, e.dst, e.kind) for e in delta[:2]] == [(0, 3, "partial_out"), (0, 3, "partial_lse")]
 
 
-@pytest.mark.parametrize("dtype,d,lq", [("float32", 64, 3), ("bfloat16", 128, 1),
-                                        ("bfloat16", 128, 32)])
-def test_run_phase2_step_pool_channels(S, dtype, d, lq):
+@pytest.mark.parametrize("dtype,d,lq,tail", [("float32", 64, 3, False), ("float32", 64, 3, True),
+                                             ("bfloat16", 128, 1, False),
+                                             ("bfloat16", 128, 32, False),
+                                             ("bfloat16", 128, 32, True)])
+def test_run_phase2_step_pool_channels(S, dtype, d, lq, tail):
     """Channels that are (layer, head) views of a multi-head host pool: each channel's K2
     call streams its own kv head only (PagedKVPool.head_view); the merged output equals
-    attention over that head's rows of every host (ss/sim.py:216-237)."""
+    attention over that head's rows of every host (ss/sim.py:216-237), with the query
+    host's own-tail causal mask over its last l_q rows when tail (ss/sim.py:195-200)."""
     dt = getattr(torch, dtype)
     rng = np.random.default_rng(5)
     layers, hkv, n_hosts = 2, 4, 3
@@ -144,7 +147,11 @@ def test_run_phase2_step_pool_channels(S, dtype, d, lq):
                                 for li in range(layers) for h in range(hkv)], pool=pool))
     qs = [torch.tensor(rng.uniform(-1, 1, (lq, d)).astype(np.float32)).to(dt).cuda()
           for _ in range(layers * hkv)]
-    outs, _ = S.run_phase2_step(hosts, qs)
+    outs, _ = S.run_phase2_step(hosts, qs, own_tail=lq if tail else 0)
+    n_keys = sum(rows)
+    keep = np.ones((lq, n_keys), dtype=bool)
+    if tail:  # the query host is the last host: its last lq rows are the query's own rows
+        keep[:, n_keys - lq:] = np.tril(np.ones((lq, lq), dtype=bool))
     # bf16: the kernel bound (2e-3) plus the rounding of the merged output to the query
     # dtype (half an ulp, 2^-9 relative)
     tol = 1e-5 if dtype == "float32" else 2e-3 + 2.0 ** -9
@@ -152,7 +159,8 @@ def test_run_phase2_step_pool_channels(S, dtype, d, lq):
         li, h = divmod(c, hkv)
         ref, _ = O.partial_attention(qc.float().cpu().numpy().astype(np.float64),
                                      np.concatenate([k[li, :, h] for k, _ in dense]).astype(np.float64),
-                                     np.concatenate([v[li, :, h] for _, v in dense]).astype(np.float64))
+                                     np.concatenate([v[li, :, h] for _, v in dense]).astype(np.float64),
+                                     mask=keep)
         err = np.abs(o.float().cpu().numpy() - ref).max() / np.abs(ref).max()
         assert err <= tol, (c, err)
 
