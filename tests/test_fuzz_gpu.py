@@ -131,3 +131,47 @@ def test_phase2_random_shapes(ops, case):
                 err = _normwise(got[b, :, h], ref)
                 assert err <= BF16_TOL, (case, hq, hkv, d, lq, lens, own_tail, splits, b, h, err)
                 assert np.abs(got_lse[b, :, h] - ref_lse).max() <= BF16_TOL, (case, b, h)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_fused_decode_random_chains(ops, case):
+    """A random multi-token decode chain through star_phase2_decode + star_decode_advance is
+    BIT-IDENTICAL, token by token, to star_kv_append + star_phase2_partial (pages, out, lse):
+    batch 1-4, G 1-8, d 64/128, ragged starting lengths (empty caches, page and tile edges),
+    auto or explicit split counts, 1-6 tokens."""
+    rng = np.random.default_rng(3000 + case)
+    hq, hkv = [(32, 8), (8, 2), (8, 8), (16, 2), (64, 8)][rng.integers(5)]
+    d = int(rng.choice([64, 128]))
+    B = int(rng.integers(1, 5))
+    page = 128
+    edges = [0, 63, 64, 127, 128, 4095, 4096]
+    starts = [int(rng.choice(edges)) if rng.random() < 0.5 else int(rng.integers(0, 6000))
+              for _ in range(B)]
+    n_tok = int(rng.integers(1, 7))
+    splits = 0 if rng.random() < 0.6 else int(rng.integers(1, 9))
+    maxk = max(starts) + n_tok + 64
+    pps = -(-maxk // page)
+    gen = torch.Generator().manual_seed(case)
+    dev = torch.device("cuda")
+    table = torch.from_numpy(rng.permutation(B * pps).astype(np.int32).reshape(B, pps)).cuda()
+    kp = ops.prng_fill((B * pps, hkv, page, d), 10 + case, 1, 1.0, torch.bfloat16, dev)
+    vp = ops.prng_fill((B * pps, hkv, page, d), 50 + case, 1, 1.0, torch.bfloat16, dev)
+    kp_r, vp_r = kp.clone(), vp.clone()
+    kl = torch.tensor(starts, dtype=torch.int32).cuda()
+    kl_r = kl.clone()
+    pos = torch.tensor([s + 3 for s in starts], dtype=torch.int64).cuda()
+    pos_r = pos.clone()
+    for t in range(n_tok):
+        q = torch.randn(B, hq, d, generator=gen).bfloat16().cuda()
+        k = torch.randn(B, hkv, d, generator=gen).bfloat16().cuda()
+        v = torch.randn(B, hkv, d, generator=gen).bfloat16().cuda()
+        qr = ops.kv_append(q, k, v, pos_r, kl_r, kp_r, vp_r, table)
+        o_r, l_r = ops.phase2_partial(qr.view(B, 1, hq, d), kp_r, vp_r, table, kl_r, maxk,
+                                      n_splits=splits)
+        pos_r += 1
+        o, l = ops.phase2_decode(q, k, v, pos, kp, vp, table, kl, maxk, n_splits=splits)
+        ops.decode_advance(kl, pos)
+        torch.cuda.synchronize()
+        assert torch.equal(o, o_r) and torch.equal(l, l_r), (case, t)
+        assert torch.equal(kl, kl_r) and torch.equal(pos, pos_r), (case, t)
+    assert torch.equal(kp, kp_r) and torch.equal(vp, vp_r), case
