@@ -98,7 +98,7 @@ __device__ long long g_k1_trace[2 * kTrTiles * 5 + kTrTiles * 2 * 2 + 2 * kTrTil
 
 
 template <int D, int NQ, int POLY, int SUM, bool SPLIT, bool L12 = false, int WAIT = 0,
-          bool MW2 = false, int SWAIT = -1, bool BATCH = false>
+          bool MW2 = false, int SWAIT = -1, bool BATCH = false, bool MC = false>
 __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>::kThreads, 1)
     phase1_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                      const __grid_constant__ CUtensorMap tm_k,
@@ -143,12 +143,18 @@ __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>:
   const int q_row0 = (int)prm.segs.q_row0[s];
   const int k_row0 = (int)prm.segs.k_row0[s];
   const int nkv = qt + 1;  // causal, q and k aligned at row 0 of the segment
+  // MC: the CTA is one of a 2-CTA cluster whose CTAs run the two head pairs of the same
+  // (segment, kv head, q tile) — the 1-D raster puts them at bx, bx + 1.  Each CTA loads one
+  // 64-column slab of every K / V tile and multicasts it to both, so each tile leaves L2 once
+  // per pair; a stage is refilled once BOTH CTAs' MMAs released it (empty count 2).
+  static_assert(!MC || (D == 128 && NQ == 2 && !MW2), "multicast pairs two D = 128 head pairs");
+  const uint32_t crank = MC ? cluster_ctarank() : 0u;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     // MW2: each q head's MMAs come from its own warp, and both release the K/V stages
-    for (int i = 0; i < C::KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], MW2 ? 2 : 1); }
-    for (int i = 0; i < C::VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], MW2 ? 2 : 1); }
+    for (int i = 0; i < C::KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], (MW2 || MC) ? 2 : 1); }
+    for (int i = 0; i < C::VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], (MW2 || MC) ? 2 : 1); }
     for (int i = 0; i < NQ; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
@@ -169,6 +175,7 @@ __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>:
   if (is_producer) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync();  // the peer's barriers are initialised before any multicast lands
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
@@ -202,9 +209,13 @@ __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>:
         const int st = j % C::KST;
         if (j >= C::KST) mbar_wait(&k_empty[st], ((j / C::KST) + 1) & 1);
         mbar_expect_tx(&k_full[st], C::kTile);
-        for (int a = 0; a < C::kSlabs; ++a)
-          tma_load_3d(smem + C::kKOff + st * C::kTile + a * C::kSlab, &tm_k, &k_full[st], a * 64,
-                      kvh, k_row0 + j * C::BN);
+        if (MC)
+          tma_load_3d_mc(smem + C::kKOff + st * C::kTile + crank * C::kSlab, &tm_k, &k_full[st],
+                         crank * 64, kvh, k_row0 + j * C::BN, 0x3);
+        else
+          for (int a = 0; a < C::kSlabs; ++a)
+            tma_load_3d(smem + C::kKOff + st * C::kTile + a * C::kSlab, &tm_k, &k_full[st], a * 64,
+                        kvh, k_row0 + j * C::BN);
       }
     } else if (lane == 1) {
       // ================= V producer =================
@@ -213,9 +224,13 @@ __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>:
         const int st = j % C::VST;
         if (j >= C::VST) mbar_wait(&v_empty[st], ((j / C::VST) + 1) & 1);
         mbar_expect_tx(&v_full[st], C::kTile);
-        for (int a = 0; a < C::kSlabs; ++a)
-          tma_load_3d(smem + C::kVOff + st * C::kTile + a * C::kSlab, &tm_v, &v_full[st], a * 64,
-                      kvh, k_row0 + j * C::BN);
+        if (MC)
+          tma_load_3d_mc(smem + C::kVOff + st * C::kTile + crank * C::kSlab, &tm_v, &v_full[st],
+                         crank * 64, kvh, k_row0 + j * C::BN, 0x3);
+        else
+          for (int a = 0; a < C::kSlabs; ++a)
+            tma_load_3d(smem + C::kVOff + st * C::kTile + a * C::kSlab, &tm_v, &v_full[st], a * 64,
+                        kvh, k_row0 + j * C::BN);
       }
     }
   };
@@ -247,7 +262,13 @@ __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>:
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
       for (int i = i0; i < i1; ++i) issue_s(i, 0);
-      if (C::KST < nkv) umma_commit_warp(&k_empty[0]);
+      auto release = [&](uint64_t* bar) {
+        if (MC)
+          umma_commit_mc_warp(bar, 0x3);
+        else
+          umma_commit_warp(bar);
+      };
+      if (C::KST < nkv) release(&k_empty[0]);
       for (int j = 0; j < nkv; ++j) {
         const int vs = j % C::VST;
         cwait(&v_full[vs], (j / C::VST) & 1, 7);
@@ -297,8 +318,8 @@ __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>:
         }
         // release a stage only if the producer will refill it (a commit nobody waits for
         // could still be in flight when the CTA exits)
-        if (j + C::VST < nkv) umma_commit_warp(&v_empty[vs]);
-        if (next && j + 1 + C::KST < nkv) umma_commit_warp(&k_empty[ks]);
+        if (j + C::VST < nkv) release(&v_empty[vs]);
+        if (next && j + 1 + C::KST < nkv) release(&k_empty[ks]);
       }
     }
   };
@@ -455,6 +476,7 @@ __global__ void __launch_bounds__(L12 ? P1Cfg<D, NQ>::kThreads12 : P1Cfg<D, NQ>:
   }
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync();  // no multicast or remote arrival targets an exited CTA
   if (is_producer) {
     __syncwarp();
     tmem_free<C::kTmemCols>(tbase);
@@ -541,7 +563,21 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
     kern = phase1_tc_kernel<D, NQ, 4, 2, true, false, 1, false, 0>;
     threads = C::kThreads;
   }
+  // K/V tiles multicast across the two head pairs of a q tile (2-CTA cluster) when the GQA
+  // ratio gives an even number of head pairs; STAR_K1_MC=0 turns it off (measurement knob)
+  bool mc = false;
+  if constexpr (NQ == 2 && D == 128) {
+    const char* ev = getenv("STAR_K1_MC");
+    if ((hq / hkv / NQ) % 2 == 0 && !(ev != nullptr && ev[0] == '0')) {
+      kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0, true, true>;
+      mc = true;
+    }
+  }
   if (const char* sv = getenv("STAR_K1_SM")) {  // measurement knob (tools/phase1_bench.py)
+    if constexpr (NQ == 2) {  // the knob forms are single-CTA kernels
+      if (mc) kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0, true>;
+    }
+    mc = false;
     const int vv = atoi(sv);
     if (vv == 1) {  // round-1 form: 10 warps, f32 += bf16 row sums, whole-P hand-off
       kern = phase1_tc_kernel<D, NQ, 0, 1, false>;
@@ -557,7 +593,24 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
   dim3 grid(tiles * hkv * (hq / hkv / NQ));
-  kern<<<grid, threads, C::kSmem, stream>>>(tq, tk, tv, prm);
+  if (mc) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, prm);
+    if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 cluster launch: %s", cudaGetErrorString(e));
+  } else {
+    kern<<<grid, threads, C::kSmem, stream>>>(tq, tk, tv, prm);
+  }
   STAR_LAUNCH_CHECK("phase1_tc");
   return STAR_OK;
 }

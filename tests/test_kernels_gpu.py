@@ -149,13 +149,13 @@ def test_phase1_tensor_core_bf16(ops, d, hq, hkv, seg_lens):
 @pytest.mark.parametrize("knob,value", [("STAR_K1_SM", "1"), ("STAR_K1_SM", "2"),
                                         ("STAR_K1_SM", "3"), ("STAR_K1_SM", "4"),
                                         ("STAR_K1_SM", "5"), ("STAR_K1_SEQ", "1"),
-                                        ("STAR_K1_SEQ", "2")])
+                                        ("STAR_K1_SEQ", "2"), ("STAR_K1_MC", "0")])
 @pytest.mark.parametrize("d,hq,hkv,seg_lens", [(128, 8, 2, [128 * 3 + 17, 256]),
                                                (64, 4, 2, [200, 384, 1])])
 def test_phase1_measurement_knobs(ops, monkeypatch, knob, value, d, hq, hkv, seg_lens):
     """Every K1 form the measurement knobs select (the round-1 kernel, no FMA exp2,
-    per-MMA elect, other exp2 shares, the MUFU ping-pong) is checked against the fp64 oracle
-    like the default form."""
+    per-MMA elect, other exp2 shares, the MUFU ping-pong, no K/V multicast) is checked against
+    the fp64 oracle like the default form."""
     monkeypatch.setenv(knob, value)  # read by the launcher at every call
     q, k, v, starts = _segments_inputs(seg_lens, hq, hkv, d, torch.bfloat16, seed=d + hq + 7)
     ref, ref_lse = _oracle_segments(q, k, v, starts, hq, hkv)
