@@ -21,7 +21,9 @@ for rows in [int(x) for x in os.environ.get("QB_ROWS", "16384,131072").split(","
     for lq in [int(x) for x in os.environ.get("QB_LQ", "1,4,16,32").split(",")]:
         q = ops.prng_fill((1, lq, hq, d), 4, 1, 1.0, torch.bfloat16, dev)
         ws = ops.Phase2Workspace()
-        f = lambda: ops.phase2_partial(q, kp, vp, table, kv_len, rows, own_tail=lq, workspace=ws)  # noqa
+        ns = int(os.environ.get("QB_SPLITS", "0"))  # 0: the library's choice
+        f = lambda: ops.phase2_partial(q, kp, vp, table, kv_len, rows, own_tail=lq, workspace=ws,  # noqa
+                                       n_splits=ns)
         f()
         torch.cuda.synchronize()
         s = torch.cuda.Stream()
