@@ -115,6 +115,15 @@ __device__ __forceinline__ uint2 ld_word(const uint2* p) {
   asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "l"(p) : "memory");
   return w;
 }
+// two {value, epoch} words (16 bytes, p 16-byte aligned); each word's epoch is checked on its own
+__device__ __forceinline__ uint4 ld_word4(const uint2* p) {
+  uint4 w;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "l"(p)
+               : "memory");
+  return w;
+}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -285,13 +285,20 @@ __device__ void exchange_merge_slice(int b, int kvh, int r_lo, int lq, int hq, i
 // not started.  Against the arrival-counter fix-up this removes the fence + atomic + fence
 // round and spreads the one-CTA merge tail (two load rounds + fold) over the group
 // (tools/k2_trace.py: 16K rows, last split stored -> exit 3.8 us -> see DESIGN §3 K2).
-template <int D, int NT>
+template <int D, int NT, int EG = 1>
 __device__ void split_merge_words(int b, int kvh, int r_lo, int r_n, int lq, int hq, int G,
                                   const uint2* w_out,
                                   const uint2* w_lse, int64_t part_rows, uint32_t es,
                                   float* final_out, float* final_lse, uint32_t* grp_epoch,
                                   const PeerPush& pp) {
-  constexpr int PS = 16;  // splits per load round (16 lse + 16 out words in flight)
+  // EG consecutive output elements of one row per thread (EG = 4: the query encode's 128-row
+  // slices): the row's lse words are loaded once and the out words as 16-byte pairs, so each
+  // thread has all its loads of a split round in flight together (EG = 1: the decode form).
+  // The per-element arithmetic (and so the result) does not depend on EG.
+  static_assert(EG == 1 || (EG == 4 && D % 4 == 0), "element groups of 1 or 4");
+  // splits per load round (PS lse + PS x EG out words in flight; 8 x 4 keeps the query
+  // encode's fold inside the registers the 12-warp layout leaves)
+  constexpr int PS = EG == 1 ? 16 : 8;
   const int tid = threadIdx.x;
   const int nsp = gridDim.x;
   const int total = r_n * D;
@@ -301,25 +308,50 @@ __device__ void split_merge_words(int b, int kvh, int r_lo, int r_n, int lq, int
   // every CTA reads the box epoch, also one whose slice is empty (lo >= hi): it still counts
   // as an arrival in exchange_merge_slice, and if it arrives last it stores this epoch back
   const uint32_t ep = pp.L.world ? exchange_epoch(pp) : 0u;
-  for (int e = lo + tid; e < hi; e += NT) {
-    const int rr = r_lo + e / D, c = e % D;
+  // groups of EG elements aligned to EG (a group never crosses a row: D % EG == 0); only the
+  // elements inside [lo, hi) are this CTA's
+  const int g_lo = lo / EG, g_hi = (hi + EG - 1) / EG;
+  for (int g = (lo < hi ? g_lo : g_hi) + tid; g < g_hi; g += NT) {
+    const int e0 = g * EG;
+    const int rr = r_lo + e0 / D, c = e0 % D;
     const int64_t orow = ((int64_t)b * lq + rr / G) * hq + kvh * G + rr % G;
-    float m = -INFINITY, acc = 0.f, o = 0.f;
+    bool in[EG];
+#pragma unroll
+    for (int k = 0; k < EG; ++k) in[k] = e0 + k >= lo && e0 + k < hi;
+    float m = -INFINITY, acc = 0.f, o[EG];
+#pragma unroll
+    for (int k = 0; k < EG; ++k) o[k] = 0.f;
     for (int p0 = 0; p0 < nsp; p0 += PS) {
-      float lv[PS], ov[PS];
+      float lv[PS], ov[PS][EG];
       uint64_t t0 = 0;
       for (;;) {
         bool all = true;
 #pragma unroll
         for (int u = 0; u < PS; ++u) {
-          uint2 wl = make_uint2(__float_as_uint(-INFINITY), es), wo = make_uint2(0u, es);
+          uint2 wl = make_uint2(__float_as_uint(-INFINITY), es);
+          uint2 wo[EG];
+#pragma unroll
+          for (int k = 0; k < EG; ++k) wo[k] = make_uint2(0u, es);
           if (p0 + u < nsp) {
             wl = ld_word(w_lse + (p0 + u) * part_rows + orow);
-            wo = ld_word(w_out + ((p0 + u) * part_rows + orow) * D + c);
+            const uint2* src = w_out + ((p0 + u) * part_rows + orow) * D + c;
+            if (EG == 4) {
+              const uint4 a = ld_word4(src), bq = ld_word4(src + 2);
+              wo[0] = make_uint2(a.x, a.y);
+              wo[EG > 1 ? 1 : 0] = make_uint2(a.z, a.w);
+              wo[EG > 2 ? 2 : 0] = make_uint2(bq.x, bq.y);
+              wo[EG > 3 ? 3 : 0] = make_uint2(bq.z, bq.w);
+            } else {
+              wo[0] = ld_word(src);
+            }
           }
-          all &= (wl.y == es) & (wo.y == es);
+          all &= (wl.y == es);
           lv[u] = __uint_as_float(wl.x);
-          ov[u] = __uint_as_float(wo.x);
+#pragma unroll
+          for (int k = 0; k < EG; ++k) {
+            all &= (!in[k]) | (wo[k].y == es);
+            ov[u][k] = __uint_as_float(wo[k].x);
+          }
         }
         if (all) break;
         if (t0 == 0) t0 = globaltimer_ns();
@@ -332,30 +364,47 @@ __device__ void split_merge_words(int b, int kvh, int r_lo, int r_n, int lq, int
           __trap();
         }
       }
-      K2_TR(e == lo && p0 == 0, 4);
+      K2_TR(g == g_lo && p0 == 0, 4);
       float mn = m;
 #pragma unroll
       for (int u = 0; u < PS; ++u) mn = fmaxf(mn, lv[u]);
       if (mn == -INFINITY) continue;  // nothing visible yet (empty splits)
       const float sc = __expf(m - mn);  // 0 while m is -inf
       acc *= sc;
-      o *= sc;
+#pragma unroll
+      for (int k = 0; k < EG; ++k) o[k] *= sc;
 #pragma unroll
       for (int u = 0; u < PS; ++u) {
         const float w = lv[u] == -INFINITY ? 0.f : __expf(lv[u] - mn);
         acc += w;
-        o = fmaf(w, ov[u], o);
+#pragma unroll
+        for (int k = 0; k < EG; ++k) o[k] = fmaf(w, ov[u][k], o[k]);
       }
       m = mn;
     }
-    put_out(pp, ep, false, final_out, orow * D + c, acc > 0.f ? o / acc : 0.f);
-    if (c == 0) put_lse(pp, ep, false, final_lse, orow, acc > 0.f ? m + __logf(acc) : -INFINITY);
+#pragma unroll
+    for (int k = 0; k < EG; ++k)
+      if (in[k]) put_out(pp, ep, false, final_out, orow * D + c + k, acc > 0.f ? o[k] / acc : 0.f);
+    if (c == 0 && in[0]) put_lse(pp, ep, false, final_lse, orow, acc > 0.f ? m + __logf(acc) : -INFINITY);
   }
   // every split's words were seen, so every CTA of the group has read the epoch: advance it
   // for the next launch (all CTAs of the group store the same value)
   if (tid == 0) grp_epoch[b * gridDim.y + blockIdx.y] = es;
   if (pp.merge)
     exchange_merge_slice<D, NT>(b, kvh, r_lo, lq, hq, G, lo, hi, ep, final_out, final_lse, pp);
+}
+
+// The query encode's fold as a separate (not inlined) function: its registers then do not
+// add to the 12-warp main loop's (inlined, the EG = 4 fold spilled there).  The decode kernel
+// keeps the inlined fold: a call measured slower at short contexts.
+template <int D, int NT, int EG>
+__device__ __noinline__ void split_merge_words_call(int b, int kvh, int r_lo, int r_n, int lq, int hq,
+                                                    int G, const uint2* w_out, const uint2* w_lse,
+                                                    int64_t part_rows, uint32_t es, float* final_out,
+                                                    float* final_lse, uint32_t* grp_epoch,
+                                                    const PeerPush& pp) {
+  split_merge_words<D, NT, EG>(b, kvh, r_lo, r_n, lq, hq, G, w_out, w_lse, part_rows, es, final_out,
+                               final_lse, grp_epoch, pp);
 }
 
 // ---- fused decode append helpers (DecodeAppend, exchange.cuh) ----
@@ -1329,8 +1378,14 @@ __global__ void __launch_bounds__(L12 ? p2q::kThreads12 : p2q::kThreads, 1) phas
     if (gridDim.x > 1) {
       // word-mode fold of the splits (+ the peer exchange push / merge when asked); it reads
       // only global words, so it runs before the CTA-wide barrier that precedes the TMEM free
-      split_merge_words<D, kSoftmaxThreads>(b, kvh, 0, QR, lq, hq, G, w_out, w_lse, part_rows, es_cta,
-                                            final_out, final_lse, grp_epoch, pp);
+      // grouped loads once every thread has >= 4 elements of the slice (l_q = 32 at G = 4:
+      // 1,024 per CTA); smaller slices keep one element per thread (more threads polling)
+      if (QR * D >= 4 * kSoftmaxThreads * (int)gridDim.x)
+        split_merge_words_call<D, kSoftmaxThreads, 4>(b, kvh, 0, QR, lq, hq, G, w_out, w_lse, part_rows,
+                                                 es_cta, final_out, final_lse, grp_epoch, pp);
+      else
+        split_merge_words_call<D, kSoftmaxThreads, 1>(b, kvh, 0, QR, lq, hq, G, w_out, w_lse, part_rows,
+                                                 es_cta, final_out, final_lse, grp_epoch, pp);
     }
   };
   if (L12) {
