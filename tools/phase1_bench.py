@@ -50,5 +50,5 @@ mhz = clk.summary()["sm_mhz"] or float("nan")
 knobs = " ".join(f"{k}={os.environ[k]}" for k in sorted(os.environ) if k.startswith("STAR_K1_"))
 print(f"{knobs or 'defaults'} ms={ms:.2f} TFLOP/s={flops / ms / 1e9:.1f} sm_mhz={mhz:.0f} "
       f"Mclk={ms * mhz / 1e3:.2f} flop/clk/SM={flops / (ms * 1e-3 * mhz * 1e6) / 148:.0f}")
-if a.save:
-    torch.save(out.cpu(), a.save)
+if a.save:  # every 61st row (all heads): enough for a bit-exact A/B without GBs on the host
+    torch.save(out[::61].cpu(), a.save)
