@@ -130,6 +130,7 @@ def _oracle_segments(q, k, v, starts, hq, hkv):
     (128, 4, 4, [300, 129]),              # MHA (one q head per CTA)
     (64, 4, 2, [200, 384, 1]),            # head_dim 64, a 1-row segment
     (128, 32, 8, [1024, 2048]),           # Llama-3.1-8B head geometry, anchor+own block shape
+    (128, 64, 8, [700, 300]),             # Llama-3.1-70B heads: 4 head pairs, 4-CTA multicast
 ])
 def test_phase1_tensor_core_bf16(ops, d, hq, hkv, seg_lens):
     q, k, v, starts = _segments_inputs(seg_lens, hq, hkv, d, torch.bfloat16, seed=d + hq)
@@ -151,6 +152,7 @@ def test_phase1_tensor_core_bf16(ops, d, hq, hkv, seg_lens):
                                         ("STAR_K1_SM", "5"), ("STAR_K1_SEQ", "1"),
                                         ("STAR_K1_SEQ", "2"), ("STAR_K1_MC", "0")])
 @pytest.mark.parametrize("d,hq,hkv,seg_lens", [(128, 8, 2, [128 * 3 + 17, 256]),
+                                               (128, 16, 2, [300, 129]),
                                                (64, 4, 2, [200, 384, 1])])
 def test_phase1_measurement_knobs(ops, monkeypatch, knob, value, d, hq, hkv, seg_lens):
     """Every K1 form the measurement knobs select (the round-1 kernel, no FMA exp2,
