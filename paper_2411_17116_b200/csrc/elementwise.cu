@@ -155,6 +155,66 @@ __global__ void rope_qkv_kernel(const T* __restrict__ qi, const T* __restrict__ 
   }
 }
 
+// bf16 form of rope_qkv_kernel with 16-byte accesses: a thread rotates 4 adjacent pairs
+// (8 elements) of one row in every head, so each load / store moves 16 bytes instead of 2.
+// The arithmetic per pair (fp64 angle and rotation, one rounding to fp32 then to bf16) is
+// rope_qkv_kernel's, so the results are bit-identical.  Needs d % 8 == 0 and 16-byte aligned
+// rows (the host checks, else the scalar kernel runs).
+__device__ __forceinline__ void rope4_bf16(uint4& w, const double (&cs)[4], const double (&sn)[4]) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&u[k]);
+    const double x0 = (double)__bfloat162float(x.x), x1 = (double)__bfloat162float(x.y);
+    __nv_bfloat162 y;
+    y.x = __float2bfloat16_rn(__double2float_rn(x0 * cs[k] - x1 * sn[k]));
+    y.y = __float2bfloat16_rn(__double2float_rn(x0 * sn[k] + x1 * cs[k]));
+    u[k] = *reinterpret_cast<const uint32_t*>(&y);
+  }
+}
+
+__global__ void rope_qkv_vec_kernel(const __nv_bfloat16* __restrict__ qi,
+                                    const __nv_bfloat16* __restrict__ ki,
+                                    const __nv_bfloat16* __restrict__ vi, __nv_bfloat16* __restrict__ qo,
+                                    __nv_bfloat16* __restrict__ ko, int64_t rows, int hq, int hkv, int d,
+                                    int64_t qis, int64_t kis, int64_t qos, int64_t kos,
+                                    const int64_t* __restrict__ pos, double theta,
+                                    const int64_t* __restrict__ cache_rows,
+                                    __nv_bfloat16* __restrict__ kp, __nv_bfloat16* __restrict__ vp,
+                                    const int32_t* __restrict__ table, int page_size) {
+  const int groups = d >> 3;  // 8-element groups per head row
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * groups) return;
+  const int64_t r = idx / groups;
+  const int g = (int)(idx - r * groups);
+  double cs[4], sn[4];
+  const double p = (double)pos[r];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = 4 * g + k;
+    sincos(p * pow(theta, -2.0 * (double)i / (double)d), &sn[k], &cs[k]);
+  }
+  const int64_t col = 8 * (int64_t)g;
+  for (int h = 0; h < hq; ++h) {
+    uint4 w = *reinterpret_cast<const uint4*>(qi + r * qis + h * d + col);
+    rope4_bf16(w, cs, sn);
+    *reinterpret_cast<uint4*>(qo + r * qos + h * d + col) = w;
+  }
+  const int64_t cr = cache_rows != nullptr ? cache_rows[r] : -1;
+  int64_t pbase = -1;
+  if (cr >= 0) pbase = ((int64_t)table[cr / page_size] * hkv * page_size + cr % page_size) * d + col;
+  for (int h = 0; h < hkv; ++h) {
+    uint4 w = *reinterpret_cast<const uint4*>(ki + r * kis + h * d + col);
+    rope4_bf16(w, cs, sn);
+    *reinterpret_cast<uint4*>(ko + r * kos + h * d + col) = w;
+    if (pbase >= 0) {
+      const int64_t po = pbase + (int64_t)h * page_size * d;
+      *reinterpret_cast<uint4*>(kp + po) = w;
+      *reinterpret_cast<uint4*>(vp + po) = *reinterpret_cast<const uint4*>(vi + r * kis + h * d + col);
+    }
+  }
+}
+
 int rope_qkv(const void* qi, const void* ki, const void* vi, int dtype, int64_t rows, int hq,
              int hkv, int d, int64_t qis, int64_t kis, void* qo, void* ko, int64_t qos,
              int64_t kos, const int64_t* pos, double theta, const int64_t* cache_rows, void* kp,
@@ -168,6 +228,19 @@ int rope_qkv(const void* qi, const void* ki, const void* vi, int dtype, int64_t 
   if (cache_rows != nullptr && (kp == nullptr || vp == nullptr || table == nullptr || page_size < 1))
     return fail(STAR_ESHAPE, "rope_qkv: cache rows given without a paged cache");
   if (rows == 0) return STAR_OK;
+  const bool vec = dtype == STAR_BF16 && d % 8 == 0 && qis % 8 == 0 && kis % 8 == 0 &&
+                   qos % 8 == 0 && kos % 8 == 0 &&
+                   (((uintptr_t)qi | (uintptr_t)ki | (uintptr_t)vi | (uintptr_t)qo | (uintptr_t)ko |
+                     (uintptr_t)kp | (uintptr_t)vp) & 15) == 0;
+  if (vec) {
+    const int64_t nv = rows * (d / 8);
+    rope_qkv_vec_kernel<<<(int)((nv + 255) / 256), 256, 0, s>>>(
+        (const __nv_bfloat16*)qi, (const __nv_bfloat16*)ki, (const __nv_bfloat16*)vi,
+        (__nv_bfloat16*)qo, (__nv_bfloat16*)ko, rows, hq, hkv, d, qis, kis, qos, kos, pos, theta,
+        cache_rows, (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, table, page_size);
+    STAR_LAUNCH_CHECK("rope_qkv");
+    return STAR_OK;
+  }
   const int64_t n = rows * (d / 2);
   const int grid = (int)((n + 255) / 256);
 #define STAR_RQKV(T)                                                                              rope_qkv_kernel<T><<<grid, 256, 0, s>>>((const T*)qi, (const T*)ki, (const T*)vi, (T*)qo,                                               (T*)ko, rows, hq, hkv, d, qis, kis, qos, kos, pos,                                              theta, cache_rows, (T*)kp, (T*)vp, table, page_size)
