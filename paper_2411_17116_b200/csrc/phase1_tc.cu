@@ -606,11 +606,27 @@ static int launch_phase1_tc(const void* q, const void* k, const void* v, SegTabl
     cfg.stream = stream;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, prm);
-    if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 cluster launch: %s", cudaGetErrorString(e));
-  } else {
-    kern<<<grid, threads, C::kSmem, stream>>>(tq, tk, tv, prm);
+    // once per process: can a 2-CTA cluster of this kernel be resident at all (a partitioned
+    // or shared GPU may not offer two free SMs of one GPC)?  If not, or if the cluster launch
+    // is refused, the single-CTA kernel runs (same results, bit for bit)
+    static int cluster_ok = -1;
+    if (cluster_ok < 0) {
+      int n = 0;
+      cluster_ok = (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) ? 1 : 0;
+      (void)cudaGetLastError();
+    }
+    e = cluster_ok ? cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, prm) : cudaErrorNotSupported;
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      mc = false;
+      if constexpr (NQ == 2) {
+        kern = phase1_tc_kernel<D, NQ, 4, 2, true, true, 1, false, 0, true>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        if (e != cudaSuccess) return fail(STAR_ECUDA, "phase1 smem attr: %s", cudaGetErrorString(e));
+      }
+    }
   }
+  if (!mc) kern<<<grid, threads, C::kSmem, stream>>>(tq, tk, tv, prm);
   STAR_LAUNCH_CHECK("phase1_tc");
   return STAR_OK;
 }
