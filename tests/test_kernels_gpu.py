@@ -487,6 +487,34 @@ def test_fused_prologue_equals_rope_plus_kv_write(ops, dtype):
     assert torch.equal(kp, kp2) and torch.equal(vp, vp2)
 
 
+def test_fused_prologue_vector_and_scalar_forms_agree(ops):
+    """The bf16 prologue runs 16-byte accesses when every row is 16-byte aligned, else the
+    one-pair-per-thread kernel: a q whose storage starts one element off (the scalar form)
+    gives the same bits as the aligned copy (the vector form), pages included."""
+    rows, hq, hkv, d, page = 260, 8, 2, 128, 64
+    rng = np.random.default_rng(12)
+    base = torch.randn(rows * hq * d + 1).bfloat16().cuda()
+    q_odd = base[1:].view(rows, hq, d)  # 2-byte aligned only
+    q_al = q_odd.clone()
+    k = torch.randn(rows, hkv, d).bfloat16().cuda()
+    v = torch.randn(rows, hkv, d).bfloat16().cuda()
+    pos = torch.from_numpy(rng.integers(0, 1 << 17, rows)).cuda()
+    cache_rows = torch.full((rows,), -1, dtype=torch.int64)
+    cache_rows[60:] = torch.arange(200)
+    cache_rows = cache_rows.cuda()
+    table = torch.tensor([2, 0, 3, 1], dtype=torch.int32).cuda()
+    outs = []
+    for q in (q_odd, q_al):
+        kp = torch.zeros((4, hkv, page, d), dtype=torch.bfloat16, device="cuda")
+        vp = torch.zeros_like(kp)
+        qo, ko = ops.rope_qkv(q, k, v, pos, cache_rows=cache_rows, k_pages=kp, v_pages=vp,
+                              page_table=table)
+        outs.append((qo, ko, kp, vp))
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(*outs))
+    assert torch.equal(outs[1][0], ops.rope(q_al, pos))
+
+
 @pytest.mark.parametrize("d,hq,hkv,dtype", [(128, 8, 2, torch.bfloat16), (64, 4, 4, torch.bfloat16),
                                             (64, 4, 2, torch.float32)])
 def test_phase1_query_range(ops, d, hq, hkv, dtype):
