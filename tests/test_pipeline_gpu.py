@@ -12,21 +12,24 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("G,rank", [(1, 0), (2, 1)])
-def test_host_pipeline_layouts_match_device_path(G, rank):
+@pytest.mark.parametrize("G,rank,L,b,a", [(1, 0, 1024, 256, 256), (2, 1, 1024, 256, 256),
+                                          # ragged last block, anchor shorter than a block
+                                          (1, 0, 1000, 256, 128), (3, 2, 1500, 384, 200)])
+def test_host_pipeline_layouts_match_device_path(G, rank, L, b, a):
     from paper_2411_17116_b200 import ops, pipeline
 
     dev = torch.device("cuda", 0)
-    L, b, a, hq, hkv, d = 1024, 256, 256, 8, 2, 128
-    n = L // b
+    hq, hkv, d = 8, 2, 128
+    n = -(-L // b)
     pos, seg, own = [], [0], []
     for i in range(n):
         if min(i * G // n, G - 1) != rank:
             continue
-        rows = list(range(a)) + list(range(i * b, i * b + b)) if i else list(range(b))
+        span = list(range(i * b, min(i * b + b, L)))
+        rows = list(range(a)) + span if i else span
         pos += rows
         seg.append(seg[-1] + len(rows))
-        own.append(b)
+        own.append(len(span))
     R = seg[-1]
     positions = torch.tensor(pos, dtype=torch.int64, device=dev)
     qf, kf, vf = (ops.prng_fill((L, h, d), s, 1, 1.0, torch.bfloat16, dev)
