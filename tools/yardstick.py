@@ -6,7 +6,8 @@ One causal self-attention over a 32,768-row augmented block (cfg2's unit: b + a 
   * cudnn    — torch SDPA, cuDNN backend (enable_gqa)
   * flash    — torch SDPA, flash backend
   * fa2      — flash_attn 2.8 flash_attn_func (GQA native)
-  * flashinfer — flashinfer.single_prefill_with_kv_cache, each backend it accepts
+  * flashinfer — flashinfer.single_prefill_with_kv_cache, each backend it accepts, and
+    flashinfer.prefill.fmha_varlen (its CUTLASS sm100a FMHA, JIT-built on first use)
 FLOPs = m(m+1)/2 pairs x Hq x 4d (the causal triangle), timed with CUDA events
 over back-to-back launches after warm-up.  Output: one JSON line (informational; library
 kernels are the yardstick, not the product).
@@ -121,6 +122,13 @@ def main():
                        lambda be=be: flashinfer.single_prefill_with_kv_cache(q, k, v, causal=True,
                                                                              backend=be),
                        check=lambda out: out)
+            from flashinfer.prefill import fmha_varlen
+
+            offs = torch.tensor([0, m], dtype=torch.int32, device=dev)
+            first = lambda out: out[0] if isinstance(out, tuple) else out  # noqa: E731
+            record("flashinfer_cutlass_sm100_fmha",
+                   lambda: fmha_varlen(q, k, v, offs, offs, causal=True),
+                   check=first)
         except ImportError as exc:
             res["kernels"]["flashinfer"] = {"error": str(exc)}
     res["clocks"] = clk.summary()
