@@ -4,7 +4,10 @@ The reference's phase 1 takes host (numpy) data and returns host data
 (ss/sim.py:126-175).  Called with pinned host tensors, this module overlaps,
 per anchor-augmented block (segment): host->device copy of block i+1, the fused
 prologue (RoPE + own-row KV page write) and K1 of block i, device->host copy of the output of block i-1 —
-on three CUDA streams ordered by events.  The copies then hide behind the
+on CUDA streams ordered by events: one for the H2D copies, one for the D2H copies and two
+for compute, taken by alternate blocks — blocks are independent (a block's K1 reads only its
+own rows), so the next block's prologue and K1 fill the SMs the current block's last CTAs
+leave idle instead of waiting for its launch to drain.  The copies then hide behind the
 tensor-core work instead of adding to it.
 
 Two host input layouts:
@@ -19,6 +22,7 @@ Two host input layouts:
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -75,7 +79,8 @@ class LayerEncodePlan:
         cr = torch.full((rows,), -1, dtype=torch.int64)
         for i, o in enumerate(own):
             cr[seg[i + 1] - o:seg[i + 1]] = torch.arange(c0[i], c0[i] + o)
-        streams = tuple(torch.cuda.Stream(device) for _ in range(3))
+        # H2D, compute (even blocks), D2H, compute (odd blocks)
+        streams = tuple(torch.cuda.Stream(device) for _ in range(4))
         return cls(list(seg), list(own), c0, q, k, v, torch.empty_like(q), torch.empty_like(k),
                    torch.empty_like(q), cr.to(device), streams)
 
@@ -162,17 +167,19 @@ def _encode(plan: LayerEncodePlan, copy_in, positions, k_pages, v_pages, page_ta
     call's H2D (fill) overlaps this call's last D2H (drain) and compute; cross-call hazards on
     the staging and output rows are ordered per segment by events (plan.comp_done / d2h_done).
     The caller then waits on plan.done (an event) or calls plan.synchronize()."""
-    s_in, s_comp, s_out = plan.streams
+    s_in, s_comp0, s_out, s_comp1 = plan.streams
+    comps = (s_comp0, s_comp1) if os.environ.get("STAR_E2E_COMP1", "0") != "1" else (s_comp0,)
     cur = torch.cuda.current_stream(plan.q.device)
     start = torch.cuda.Event()
     start.record(cur)
-    for st in (s_in, s_comp, s_out):
+    for st in (s_in, s_out) + comps:
         st.wait_event(start)
     n = len(plan.seg) - 1
     if len(plan.comp_done) != n:
         plan.comp_done, plan.d2h_done = [None] * n, [None] * n
     for i in range(n):
         a, b = plan.seg[i], plan.seg[i + 1]
+        s_comp = comps[i % len(comps)]
         cuts = _cuts(b - a, i == 0, i == n - 1)
         for k_part, (p0, p1) in enumerate(zip(cuts[:-1], cuts[1:])):
             with torch.cuda.stream(s_in):
@@ -202,7 +209,8 @@ def _encode(plan: LayerEncodePlan, copy_in, positions, k_pages, v_pages, page_ta
         ev_o = torch.cuda.Event()
         ev_o.record(s_out)
         plan.d2h_done[i] = ev_o
-    s_out.wait_stream(s_comp)
+    for st in comps:
+        s_out.wait_stream(st)
     plan.done = torch.cuda.Event()
     plan.done.record(s_out)
     if wait:
