@@ -261,3 +261,29 @@ def test_epoch_counters_wrap(mods):
         torch.cuda.synchronize()
         hdr0 = int(exs[0].own_box.view(torch.int32)[0].item()) & 0xFFFFFFFF
         assert hdr0 == 4, hdr0  # 0xFFFFFFFF, 2, 3, 4
+
+
+def _random_exchange_cases(n):
+    rng = np.random.default_rng(4242)
+    cases = []
+    for _ in range(n):
+        world = int(rng.integers(1, 9))
+        hq, hkv = [(32, 8), (8, 2), (8, 8), (16, 4)][rng.integers(4)]
+        d = int(rng.choice([64, 128]))
+        lq = int(rng.choice([1, 4, 8, 32]))
+        lens = [0 if rng.random() < 0.2 else int(rng.integers(max(lq, 1), 9000)) for _ in range(world)]
+        if not any(lens):
+            lens[-1] = int(rng.integers(lq, 9000))
+        splits = int(rng.choice([0, 0, 1, 2, 4]))
+        dtype = torch.float32 if rng.random() < 0.3 else torch.bfloat16
+        cases.append((dtype, world, lens, hq, hkv, d, splits, lq))
+    return cases
+
+
+@pytest.mark.parametrize("case", _random_exchange_cases(10))
+def test_exchange_random_shapes(mods, case):
+    """A seeded random sweep of the fused exchange (1-8 ranks, empty ranks, GQA 1-4, d 64/128,
+    query encodes of 1-32 rows incl. the K2q path, explicit and automatic splits, fp32 and
+    bf16): the same bit-exact and oracle checks as the fixed cases above."""
+    dtype, world, lens, hq, hkv, d, splits, lq = case
+    test_exchange_matches_unfused_and_oracle(mods, dtype, world, lens, hq, hkv, d, splits, lq)
